@@ -1,0 +1,406 @@
+// api.cu -- the extern "C" boundary (include/bolt.h): argument validation,
+// status codes, thread-local error text, workspace sizing and dispatch to the
+// sm_100a kernels.  No allocation, no synchronization, no torch types.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+
+#include "common.cuh"
+
+using namespace bolt;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+bolt_status fail(bolt_status st, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+bolt_status cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return BOLT_OK;
+    return fail(BOLT_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+struct DevInfo {
+    int ok;   // 1 = sm_100, 0 = unsupported
+    int sms;
+};
+std::atomic<int> g_dev_cache[64];  // 0 unknown, else (sms << 2) | (ok << 1) | 1
+
+bolt_status device_info(DevInfo* info) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+    int cached = (dev >= 0 && dev < 64) ? g_dev_cache[dev].load(std::memory_order_relaxed) : 0;
+    if (!cached) {
+        int major = 0, minor = 0, sms = 0;
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
+        const int ok = (major == 10 && minor == 0) ? 1 : 0;
+        cached = (sms << 2) | (ok << 1) | 1;
+        if (dev >= 0 && dev < 64) g_dev_cache[dev].store(cached, std::memory_order_relaxed);
+    }
+    info->ok = (cached >> 1) & 1;
+    info->sms = cached >> 2;
+    if (!info->ok) return fail(BOLT_E_DEVICE, "device %d is not sm_100 (B200); this library is sm_100a only", dev);
+    return BOLT_OK;
+}
+
+int sms_or_default() {
+    DevInfo d{};
+    if (device_info(&d) != BOLT_OK) return 148;
+    return d.sms;
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+bolt_status check_m(int m) {
+    if (m < 1 || m > kMaxM) return fail(BOLT_E_SHAPE, "m = %d outside 1..64", m);
+    return BOLT_OK;
+}
+
+bolt_status check_jm(int j, int m) {
+    if (bolt_status st = check_m(m)) return st;
+    if (j < 1) return fail(BOLT_E_SHAPE, "j = %d < 1", j);
+    if (j % m) return fail(BOLT_E_SHAPE, "j = %d not divisible by m = %d (zero-pad to a multiple)", j, m);
+    return BOLT_OK;
+}
+
+#define TRY(x)                                \
+    do {                                      \
+        bolt_status _st = (x);                \
+        if (_st != BOLT_OK) return _st;       \
+    } while (0)
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ---- top-k plan shared by workspace sizing and execution
+struct TopkPlan {
+    int variant;   // resolved PRMT / TC
+    int parts;
+    size_t ws;
+};
+
+TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
+    TopkPlan p{};
+    int v = variant;
+    if (v == BOLT_VARIANT_AUTO) v = topk_tc_supported(n, m, nq, k) && nq >= 64 ? BOLT_VARIANT_TC : BOLT_VARIANT_PRMT;
+    p.variant = v;
+    p.parts = v == BOLT_VARIANT_TC ? topk_tc_parts(n, m, nq, k, sms) : topk_prmt_parts(n, m, nq, k, sms);
+    p.ws = p.parts > 1 ? (size_t)p.parts * nq * k * sizeof(uint64_t) : 0;
+    return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bolt_version(void) { return "bolt-b200 1.0 (abi 1, sm_100a)"; }
+
+const char* bolt_last_error(void) { return g_err; }
+
+int64_t bolt_codes_words(int64_t n, int m) {
+    if (n < 0 || m < 1 || m > kMaxM) return -1;
+    return ceil_div(n, kRowsPerWord) * m;
+}
+
+bolt_status bolt_encode(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,
+                        uint32_t* codes, bolt_stream_t stream) {
+    TRY(check_jm(j, m));
+    if (n < 0) return fail(BOLT_E_SHAPE, "n = %lld < 0", (long long)n);
+    if (ldx < j) return fail(BOLT_E_SHAPE, "ldx = %lld < j = %d", (long long)ldx, j);
+    if (j > 2048) return fail(BOLT_E_SHAPE, "j = %d > 2048 (centroids must fit in shared memory)", j);
+    if (n == 0) return BOLT_OK;
+    if (!X || !C || !codes) return fail(BOLT_E_NULL, "bolt_encode: NULL pointer");
+    if (!aligned(C, 16)) return fail(BOLT_E_ALIGN, "bolt_encode: C must be 16-byte aligned");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_encode(X, n, j, ldx, C, m, codes, (cudaStream_t)stream), "bolt_encode");
+}
+
+bolt_status bolt_pack_codes(const uint8_t* flat, int64_t n, int m, uint32_t* codes,
+                            bolt_stream_t stream) {
+    TRY(check_m(m));
+    if (n < 0) return fail(BOLT_E_SHAPE, "n < 0");
+    if (n == 0) return BOLT_OK;
+    if (!flat || !codes) return fail(BOLT_E_NULL, "bolt_pack_codes: NULL pointer");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_pack(flat, n, m, codes, (cudaStream_t)stream), "bolt_pack_codes");
+}
+
+bolt_status bolt_unpack_codes(const uint32_t* codes, int64_t n, int m, uint8_t* flat,
+                              bolt_stream_t stream) {
+    TRY(check_m(m));
+    if (n < 0) return fail(BOLT_E_SHAPE, "n < 0");
+    if (n == 0) return BOLT_OK;
+    if (!flat || !codes) return fail(BOLT_E_NULL, "bolt_unpack_codes: NULL pointer");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_unpack(codes, n, m, flat, (cudaStream_t)stream), "bolt_unpack_codes");
+}
+
+static bolt_status lut_common(const float* Q, int64_t nq, int j, int64_t ldq, const float* C, int m,
+                              bolt_metric metric) {
+    TRY(check_jm(j, m));
+    if (nq < 0) return fail(BOLT_E_SHAPE, "nq < 0");
+    if (ldq < j) return fail(BOLT_E_SHAPE, "ldq = %lld < j = %d", (long long)ldq, j);
+    if (metric != BOLT_L2SQ && metric != BOLT_DOT) return fail(BOLT_E_RANGE, "metric %d", (int)metric);
+    if (nq > 0 && (!Q || !C)) return fail(BOLT_E_NULL, "NULL query/centroid pointer");
+    return BOLT_OK;
+}
+
+bolt_status bolt_build_luts(const float* Q, int64_t nq, int j, int64_t ldq, const float* C, int m,
+                            bolt_metric metric, float* luts, bolt_stream_t stream) {
+    TRY(lut_common(Q, nq, j, ldq, C, m, metric));
+    if (nq == 0) return BOLT_OK;
+    if (!luts) return fail(BOLT_E_NULL, "luts NULL");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_build_luts(Q, nq, j, ldq, C, m, metric, 1.f, nullptr, nullptr, luts,
+                                         nullptr, (cudaStream_t)stream), "bolt_build_luts");
+}
+
+bolt_status bolt_build_luts_f64(const float* Q, int64_t nq, int j, int64_t ldq, const float* C,
+                                int m, bolt_metric metric, double* luts, bolt_stream_t stream) {
+    TRY(lut_common(Q, nq, j, ldq, C, m, metric));
+    if (nq == 0) return BOLT_OK;
+    if (!luts) return fail(BOLT_E_NULL, "luts NULL");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_build_luts(Q, nq, j, ldq, C, m, metric, 1.f, nullptr, nullptr, nullptr,
+                                         luts, (cudaStream_t)stream), "bolt_build_luts_f64");
+}
+
+bolt_status bolt_quantize_luts(const float* luts, int64_t nq, int m, float a, const float* b,
+                               uint8_t* qluts, bolt_stream_t stream) {
+    TRY(check_m(m));
+    if (nq < 0) return fail(BOLT_E_SHAPE, "nq < 0");
+    if (!(a > 0.f)) return fail(BOLT_E_RANGE, "a = %g must be > 0", (double)a);
+    if (nq == 0) return BOLT_OK;
+    if (!luts || !b || !qluts) return fail(BOLT_E_NULL, "bolt_quantize_luts: NULL pointer");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_quantize(luts, nq, m, a, b, qluts, (cudaStream_t)stream), "bolt_quantize_luts");
+}
+
+bolt_status bolt_build_quantized_luts(const float* Q, int64_t nq, int j, int64_t ldq, const float* C,
+                                      int m, bolt_metric metric, float a, const float* b,
+                                      uint8_t* qluts, float* luts_or_null, bolt_stream_t stream) {
+    TRY(lut_common(Q, nq, j, ldq, C, m, metric));
+    if (!(a > 0.f)) return fail(BOLT_E_RANGE, "a = %g must be > 0", (double)a);
+    if (nq == 0) return BOLT_OK;
+    if (!b || !qluts) return fail(BOLT_E_NULL, "bolt_build_quantized_luts: NULL pointer");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_build_luts(Q, nq, j, ldq, C, m, metric, a, b, qluts, luts_or_null,
+                                         nullptr, (cudaStream_t)stream), "bolt_build_quantized_luts");
+}
+
+static bolt_status scan_common(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts,
+                               int64_t nq) {
+    TRY(check_m(m));
+    if (n < 0 || nq < 0) return fail(BOLT_E_SHAPE, "n or nq < 0");
+    if (n > 0 && nq > 0) {
+        if (!codes || !qluts) return fail(BOLT_E_NULL, "codes/qluts NULL");
+        if (!aligned(codes, 16)) return fail(BOLT_E_ALIGN, "codes must be 16-byte aligned");
+        if (!aligned(qluts, 16)) return fail(BOLT_E_ALIGN, "qluts must be 16-byte aligned");
+    }
+    return BOLT_OK;
+}
+
+bolt_status bolt_scan(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts, int64_t nq,
+                      uint16_t* out, int64_t ldo, bolt_stream_t stream) {
+    TRY(scan_common(codes, n, m, qluts, nq));
+    if (ldo < nq) return fail(BOLT_E_SHAPE, "ldo = %lld < nq = %lld", (long long)ldo, (long long)nq);
+    if (n == 0 || nq == 0) return BOLT_OK;
+    if (!out) return fail(BOLT_E_NULL, "out NULL");
+    DevInfo d;
+    TRY(device_info(&d));
+    ScanArgs a{codes, n, ceil_div(n, 8), m, qluts, nq};
+    return cuda_status(launch_scan_full(a, out, nullptr, ldo, 0.f, 0.f, (cudaStream_t)stream), "bolt_scan");
+}
+
+bolt_status bolt_scan_dequant(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts,
+                              int64_t nq, float a, float b_sum, float* out, int64_t ldo,
+                              bolt_stream_t stream) {
+    TRY(scan_common(codes, n, m, qluts, nq));
+    if (ldo < nq) return fail(BOLT_E_SHAPE, "ldo = %lld < nq = %lld", (long long)ldo, (long long)nq);
+    if (!(a > 0.f)) return fail(BOLT_E_RANGE, "a = %g must be > 0", (double)a);
+    if (n == 0 || nq == 0) return BOLT_OK;
+    if (!out) return fail(BOLT_E_NULL, "out NULL");
+    DevInfo d;
+    TRY(device_info(&d));
+    ScanArgs sa{codes, n, ceil_div(n, 8), m, qluts, nq};
+    return cuda_status(launch_scan_full(sa, nullptr, out, ldo, 1.0f / a, b_sum, (cudaStream_t)stream),
+                       "bolt_scan_dequant");
+}
+
+size_t bolt_topk_workspace_bytes_ex(int64_t n, int m, int64_t nq, int k, int variant) {
+    if (n < 0 || nq < 0 || k < 1 || k > kMaxK || m < 1 || m > kMaxM) return 0;
+    return topk_plan(n, m, nq, k, variant, sms_or_default()).ws;
+}
+
+size_t bolt_topk_workspace_bytes(int64_t n, int m, int64_t nq, int k) {
+    return bolt_topk_workspace_bytes_ex(n, m, nq, k, BOLT_VARIANT_AUTO);
+}
+
+bolt_status bolt_topk_ex(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts,
+                         int64_t nq, int k, bolt_metric metric, int64_t index_base,
+                         uint64_t* out_keys, void* ws, size_t ws_bytes, int variant,
+                         bolt_stream_t stream) {
+    TRY(scan_common(codes, n, m, qluts, nq));
+    if (k < 1 || k > kMaxK) return fail(BOLT_E_SHAPE, "k = %d outside 1..128", k);
+    if (metric != BOLT_L2SQ && metric != BOLT_DOT) return fail(BOLT_E_RANGE, "metric %d", (int)metric);
+    if (variant < BOLT_VARIANT_AUTO || variant > BOLT_VARIANT_TC) return fail(BOLT_E_RANGE, "variant %d", variant);
+    if (index_base < 0 || index_base + n >= (int64_t(1) << 48))
+        return fail(BOLT_E_RANGE, "index_base + n must be < 2^48");
+    if (nq == 0) return BOLT_OK;
+    if (!out_keys) return fail(BOLT_E_NULL, "out_keys NULL");
+    DevInfo d;
+    TRY(device_info(&d));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0)
+        return cuda_status(cudaMemsetAsync(out_keys, 0xFF, (size_t)nq * k * sizeof(uint64_t), s), "bolt_topk");
+    if (variant == BOLT_VARIANT_TC && !topk_tc_supported(n, m, nq, k))
+        return fail(BOLT_E_RANGE, "tcgen05 variant does not support m=%d k=%d", m, k);
+    TopkPlan p = topk_plan(n, m, nq, k, variant, d.sms);
+    if (p.ws > 0 && (!ws || ws_bytes < p.ws))
+        return fail(BOLT_E_WORKSPACE, "workspace of %zu bytes required, %zu given", p.ws, ws_bytes);
+    if (p.ws > 0 && !aligned(ws, 8)) return fail(BOLT_E_ALIGN, "workspace must be 8-byte aligned");
+    ScanArgs a{codes, n, ceil_div(n, 8), m, qluts, nq};
+    uint64_t* parts_out = p.parts > 1 ? static_cast<uint64_t*>(ws) : out_keys;
+    cudaError_t e = p.variant == BOLT_VARIANT_TC
+                        ? launch_topk_tc(a, k, metric, index_base, p.parts, parts_out, s)
+                        : launch_topk_prmt(a, k, metric, index_base, p.parts, parts_out, s);
+    if (e != cudaSuccess) return cuda_status(e, "bolt_topk scan");
+    if (p.parts > 1) return cuda_status(launch_merge(parts_out, p.parts, nq, k, out_keys, s), "bolt_topk merge");
+    return BOLT_OK;
+}
+
+bolt_status bolt_topk(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts, int64_t nq,
+                      int k, bolt_metric metric, int64_t index_base, uint64_t* out_keys, void* ws,
+                      size_t ws_bytes, bolt_stream_t stream) {
+    return bolt_topk_ex(codes, n, m, qluts, nq, k, metric, index_base, out_keys, ws, ws_bytes,
+                        BOLT_VARIANT_AUTO, stream);
+}
+
+bolt_status bolt_topk_merge(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out_keys,
+                            bolt_stream_t stream) {
+    if (w < 1 || k < 1 || nq < 0) return fail(BOLT_E_SHAPE, "w, k must be >= 1, nq >= 0");
+    if ((int64_t)w * k > 8192) return fail(BOLT_E_SHAPE, "w*k = %lld > 8192", (long long)w * k);
+    if (nq == 0) return BOLT_OK;
+    if (!keys || !out_keys) return fail(BOLT_E_NULL, "bolt_topk_merge: NULL pointer");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_merge(keys, w, nq, k, out_keys, (cudaStream_t)stream), "bolt_topk_merge");
+}
+
+bolt_status bolt_keys_split(const uint64_t* keys, int64_t count, bolt_metric metric,
+                            uint16_t* vals, int64_t* idx, bolt_stream_t stream) {
+    if (count < 0) return fail(BOLT_E_SHAPE, "count < 0");
+    if (metric != BOLT_L2SQ && metric != BOLT_DOT) return fail(BOLT_E_RANGE, "metric %d", (int)metric);
+    if (count == 0) return BOLT_OK;
+    if (!keys || (!vals && !idx)) return fail(BOLT_E_NULL, "bolt_keys_split: NULL pointer");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_keys_split(keys, count, metric, vals, idx, (cudaStream_t)stream), "bolt_keys_split");
+}
+
+// ------------------------------------------------------------ host search
+size_t bolt_search_host_workspace_bytes(int64_t n, int j, int m, int64_t nq, int k) {
+    if (n < 0 || nq < 0 || j < 1 || m < 1 || m > kMaxM || k < 1 || k > kMaxK) return 0;
+    size_t s = 0;
+    s += align256((size_t)n * j * sizeof(float));
+    s += align256((size_t)nq * j * sizeof(float));
+    s += align256((size_t)ceil_div(n, 8) * m * sizeof(uint32_t));
+    s += align256((size_t)nq * m * kK);
+    s += align256((size_t)nq * k * sizeof(uint64_t));
+    s += align256(bolt_topk_workspace_bytes(n, m, nq, k));
+    return s;
+}
+
+bolt_status bolt_search_host(const float* X_host, int64_t n, int j, const float* Q_host,
+                             int64_t nq, const float* C, int m, bolt_metric metric, float a,
+                             const float* b, int k, uint64_t* keys_host, void* ws,
+                             size_t ws_bytes, bolt_stream_t stream) {
+    TRY(check_jm(j, m));
+    if (n < 1 || nq < 0) return fail(BOLT_E_SHAPE, "n must be >= 1, nq >= 0");
+    if (k < 1 || k > kMaxK) return fail(BOLT_E_SHAPE, "k = %d outside 1..128", k);
+    if (!(a > 0.f)) return fail(BOLT_E_RANGE, "a must be > 0");
+    if (nq == 0) return BOLT_OK;
+    if (!X_host || !Q_host || !C || !b || !keys_host || !ws) return fail(BOLT_E_NULL, "bolt_search_host: NULL pointer");
+    const size_t need = bolt_search_host_workspace_bytes(n, j, m, nq, k);
+    if (ws_bytes < need) return fail(BOLT_E_WORKSPACE, "workspace of %zu bytes required, %zu given", need, ws_bytes);
+    if (!aligned(ws, 256)) return fail(BOLT_E_ALIGN, "workspace must be 256-byte aligned");
+    DevInfo d;
+    TRY(device_info(&d));
+    cudaStream_t s = (cudaStream_t)stream;
+    char* p = static_cast<char*>(ws);
+    float* Xd = reinterpret_cast<float*>(p); p += align256((size_t)n * j * sizeof(float));
+    float* Qd = reinterpret_cast<float*>(p); p += align256((size_t)nq * j * sizeof(float));
+    uint32_t* codes = reinterpret_cast<uint32_t*>(p); p += align256((size_t)ceil_div(n, 8) * m * sizeof(uint32_t));
+    uint8_t* ql = reinterpret_cast<uint8_t*>(p); p += align256((size_t)nq * m * kK);
+    uint64_t* keys = reinterpret_cast<uint64_t*>(p); p += align256((size_t)nq * k * sizeof(uint64_t));
+    void* tws = p;
+    const size_t tws_bytes = bolt_topk_workspace_bytes(n, m, nq, k);
+    TRY(cuda_status(cudaMemcpyAsync(Xd, X_host, (size_t)n * j * sizeof(float), cudaMemcpyHostToDevice, s), "H2D X"));
+    TRY(cuda_status(cudaMemcpyAsync(Qd, Q_host, (size_t)nq * j * sizeof(float), cudaMemcpyHostToDevice, s), "H2D Q"));
+    TRY(bolt_encode(Xd, n, j, j, C, m, codes, stream));
+    TRY(bolt_build_quantized_luts(Qd, nq, j, j, C, m, metric, a, b, ql, nullptr, stream));
+    TRY(bolt_topk(codes, n, m, ql, nq, k, metric, 0, keys, tws, tws_bytes, stream));
+    return cuda_status(cudaMemcpyAsync(keys_host, keys, (size_t)nq * k * sizeof(uint64_t), cudaMemcpyDeviceToHost, s), "D2H keys");
+}
+
+// ------------------------------------------------------------------- fit
+size_t bolt_kmeans_workspace_bytes(int64_t n, int j, int m) {
+    if (n < 1 || j < 1 || m < 1 || m > kMaxM || j % m) return 0;
+    return kmeans_ws_bytes(n, j, m);
+}
+
+bolt_status bolt_kmeans(const float* train, int64_t n, int j, int64_t ldx, int m,
+                        const int64_t* init, int iters, float* C_out, void* ws, size_t ws_bytes,
+                        bolt_stream_t stream) {
+    TRY(check_jm(j, m));
+    if (n < kK) return fail(BOLT_E_SHAPE, "k-means needs n >= 16 rows, got %lld", (long long)n);
+    if (ldx < j) return fail(BOLT_E_SHAPE, "ldx < j");
+    if (iters < 0) return fail(BOLT_E_RANGE, "iters < 0");
+    if (j / m > 64) return fail(BOLT_E_SHAPE, "sub-vector length j/m = %d > 64", j / m);
+    if (!train || !init || !C_out) return fail(BOLT_E_NULL, "bolt_kmeans: NULL pointer");
+    const size_t need = kmeans_ws_bytes(n, j, m);
+    if (!ws || ws_bytes < need) return fail(BOLT_E_WORKSPACE, "workspace of %zu bytes required", need);
+    if (!aligned(ws, 256)) return fail(BOLT_E_ALIGN, "workspace must be 256-byte aligned");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_kmeans(train, n, j, ldx, m, init, iters, C_out, ws, (cudaStream_t)stream), "bolt_kmeans");
+}
+
+size_t bolt_calibrate_workspace_bytes(int64_t nq, int m) {
+    if (nq < 1 || m < 1 || m > kMaxM) return 0;
+    return calibrate_ws_bytes(nq, m);
+}
+
+bolt_status bolt_calibrate(const double* luts, int64_t nq, int m, float* a_out, float* b_out,
+                           double* alpha_mse_out, void* ws, size_t ws_bytes, bolt_stream_t stream) {
+    TRY(check_m(m));
+    if (nq < 1) return fail(BOLT_E_SHAPE, "nq must be >= 1");
+    if (!luts || !a_out || !b_out) return fail(BOLT_E_NULL, "bolt_calibrate: NULL pointer");
+    const size_t need = calibrate_ws_bytes(nq, m);
+    if (!ws || ws_bytes < need) return fail(BOLT_E_WORKSPACE, "workspace of %zu bytes required", need);
+    if (!aligned(ws, 256)) return fail(BOLT_E_ALIGN, "workspace must be 256-byte aligned");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_calibrate(luts, nq, m, a_out, b_out, alpha_mse_out, ws, (cudaStream_t)stream),
+                       "bolt_calibrate");
+}
+
+}  // extern "C"

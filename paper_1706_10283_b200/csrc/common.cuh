@@ -1,0 +1,91 @@
+// common.cuh -- shared device helpers of the sm_100a Bolt library.
+// (No code here is shared with oracle/; the oracle has its own C file.)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bolt.h"
+
+namespace bolt {
+
+constexpr int kK = 16;           // centroids per codebook
+constexpr int kMaxM = 64;        // codebooks
+constexpr int kRowsPerWord = 8;  // layout v1: 8 rows x 4 bits per u32 word
+constexpr int kMaxK = 128;       // top-k
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ inline int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// PRMT (byte permute, default mode): result byte i = byte sel[4i+2:4i] of
+// {hi, lo}; if sel bit 4i+3 is set the sign bit of that byte is replicated
+// instead.  Only the low 16 bits of sel are used.
+__device__ __forceinline__ uint32_t prmt(uint32_t lo, uint32_t hi, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(hi), "r"(sel));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t vminu2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
+// 64-bit ranking key (R13): smaller is better; ties -> lower global index.
+__device__ __forceinline__ uint64_t make_key(uint32_t kv, uint64_t gidx) {
+    return (static_cast<uint64_t>(kv) << 48) | gidx;
+}
+
+// Per-launch argument block for the scan kernels.
+struct ScanArgs {
+    const uint32_t* codes;
+    int64_t n;            // rows
+    int64_t groups;       // ceil(n / 8)
+    int m;
+    const uint8_t* qluts;
+    int64_t nq;
+};
+
+}  // namespace bolt
+
+// ---------------------------------------------------------------- launchers
+// Implemented in the .cu files, called by api.cu after validation.  They
+// return cudaGetLastError() of their launch.
+namespace bolt {
+cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,
+                          uint32_t* codes, cudaStream_t s);
+cudaError_t launch_pack(const uint8_t* flat, int64_t n, int m, uint32_t* codes, cudaStream_t s);
+cudaError_t launch_unpack(const uint32_t* codes, int64_t n, int m, uint8_t* flat, cudaStream_t s);
+
+cudaError_t launch_build_luts(const float* Q, int64_t nq, int j, int64_t ldq, const float* C, int m,
+                              int metric, float a, const float* b, uint8_t* qluts, float* luts32,
+                              double* luts64, cudaStream_t s);
+cudaError_t launch_quantize(const float* luts, int64_t nq, int m, float a, const float* b,
+                            uint8_t* qluts, cudaStream_t s);
+
+cudaError_t launch_scan_full(const ScanArgs& a, uint16_t* out16, float* out32, int64_t ldo,
+                             float inv_a, float b_sum, cudaStream_t s);
+
+// top-k (PRMT variant): partial lists [parts][nq][k] in ws, then merge
+int topk_prmt_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
+cudaError_t launch_topk_prmt(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
+                             uint64_t* part_keys, cudaStream_t s);
+// top-k (tcgen05 variant)
+int topk_tc_supported(int64_t n, int m, int64_t nq, int k);
+int topk_tc_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
+cudaError_t launch_topk_tc(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
+                           uint64_t* part_keys, cudaStream_t s);
+
+cudaError_t launch_merge(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out,
+                         cudaStream_t s);
+cudaError_t launch_keys_split(const uint64_t* keys, int64_t count, int metric, uint16_t* vals,
+                              int64_t* idx, cudaStream_t s);
+
+size_t kmeans_ws_bytes(int64_t n, int j, int m);
+cudaError_t launch_kmeans(const float* train, int64_t n, int j, int64_t ldx, int m,
+                          const int64_t* init, int iters, float* C_out, void* ws, cudaStream_t s);
+size_t calibrate_ws_bytes(int64_t nq, int m);
+cudaError_t launch_calibrate(const double* luts, int64_t nq, int m, float* a_out, float* b_out,
+                             double* alpha_mse, void* ws, cudaStream_t s);
+}  // namespace bolt

@@ -1,0 +1,170 @@
+// encode.cu -- h(x): 4-bit PQ encoder and the
+// layout-v1 pack/unpack helpers.
+//
+// Each thread encodes 4 consecutive rows; centroids of all codebooks sit in
+// shared memory negated and transposed ([c][dim][16]) so that one LDS.128
+// feeds 4 centroids to the 4 rows, and each (row, centroid pair) update is one
+// packed FADD2 (x + (-c) == x - c exactly) and one FFMA2 -- the same fp32
+// operations, in the same ascending-dimension order, as the scalar
+// d += (x - c)^2.  The argmin keeps the lowest index on ties (R9).  Codes of
+// a block (512 rows = 64 layout-v1 groups) are staged in shared memory and
+// written as one contiguous run of 64*m words.
+#include "common.cuh"
+
+namespace bolt {
+namespace {
+
+constexpr int kEncThreads = 128;
+constexpr int kEncRowsPerThread = 4;
+constexpr int kEncRowsPerBlock = kEncThreads * kEncRowsPerThread;  // 512
+constexpr int kEncGroupsPerBlock = kEncRowsPerBlock / kRowsPerWord;  // 64
+
+template <bool kVec>
+__global__ void __launch_bounds__(kEncThreads)
+encode_kernel(const float* __restrict__ X, int64_t n, int j, int64_t ldx,
+              const float* __restrict__ C, int m, uint32_t* __restrict__ codes) {
+    extern __shared__ float4 enc_smem4[];
+    float* cneg = reinterpret_cast<float*>(enc_smem4);  // [m][L][16] negated
+    uint32_t* stage = reinterpret_cast<uint32_t*>(cneg + (size_t)j * kK);  // [64][m]
+    const int L = j / m;
+    // C is [m][16][L]; store -C as [m][L][16]
+    for (int e = threadIdx.x; e < j * kK; e += blockDim.x) {
+        int c = e / (kK * L);
+        int r = e - c * kK * L;
+        int k = r / L;
+        int d = r - k * L;
+        cneg[((size_t)c * L + d) * kK + k] = -C[e];
+    }
+    __syncthreads();
+
+    const int64_t row0 = (int64_t)blockIdx.x * kEncRowsPerBlock + threadIdx.x * kEncRowsPerThread;
+    const float* xr[kEncRowsPerThread];
+    bool valid[kEncRowsPerThread];
+#pragma unroll
+    for (int r = 0; r < kEncRowsPerThread; ++r) {
+        valid[r] = row0 + r < n;
+        xr[r] = X + (valid[r] ? (row0 + r) : 0) * ldx;
+    }
+    for (int c = 0; c < m; ++c) {
+        float2 d[kEncRowsPerThread][kK / 2];
+#pragma unroll
+        for (int r = 0; r < kEncRowsPerThread; ++r)
+#pragma unroll
+            for (int p = 0; p < kK / 2; ++p) d[r][p] = make_float2(0.f, 0.f);
+        const float* cc = cneg + (size_t)c * L * kK;
+        for (int d0 = 0; d0 < L; d0 += 4) {
+            float xv[kEncRowsPerThread][4];
+#pragma unroll
+            for (int r = 0; r < kEncRowsPerThread; ++r) {
+                const float* p = xr[r] + c * L + d0;
+                if (kVec) {
+                    float4 v = valid[r] ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0, 0, 0, 0);
+                    xv[r][0] = v.x; xv[r][1] = v.y; xv[r][2] = v.z; xv[r][3] = v.w;
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) xv[r][t] = (valid[r] && d0 + t < L) ? __ldg(p + t) : 0.f;
+                }
+            }
+            const int dn = min(4, L - d0);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (t >= dn) break;
+                const float4* cv = reinterpret_cast<const float4*>(cc + (size_t)(d0 + t) * kK);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    float4 c4 = cv[q];
+                    float2 ca = make_float2(c4.x, c4.y), cb = make_float2(c4.z, c4.w);
+#pragma unroll
+                    for (int r = 0; r < kEncRowsPerThread; ++r) {
+                        float2 xx = make_float2(xv[r][t], xv[r][t]);
+                        float2 da = __fadd2_rn(xx, ca);
+                        float2 db = __fadd2_rn(xx, cb);
+                        d[r][2 * q] = __ffma2_rn(da, da, d[r][2 * q]);
+                        d[r][2 * q + 1] = __ffma2_rn(db, db, d[r][2 * q + 1]);
+                    }
+                }
+            }
+        }
+        // argmin, lowest index on ties; pack this thread's 4 rows (16 bits)
+        uint32_t half = 0;
+#pragma unroll
+        for (int r = 0; r < kEncRowsPerThread; ++r) {
+            float best = d[r][0].x;
+            uint32_t arg = 0;
+#pragma unroll
+            for (int p = 0; p < kK / 2; ++p) {
+                if (p > 0 && d[r][p].x < best) { best = d[r][p].x; arg = 2 * p; }
+                if (d[r][p].y < best) { best = d[r][p].y; arg = 2 * p + 1; }
+            }
+            if (!valid[r]) arg = 0;
+            half |= arg << (4 * r);
+        }
+        uint32_t other = __shfl_xor_sync(0xffffffffu, half, 1);
+        if ((threadIdx.x & 1) == 0) stage[(threadIdx.x >> 1) * m + c] = half | (other << 16);
+    }
+    __syncthreads();
+    const int64_t g0 = (int64_t)blockIdx.x * kEncGroupsPerBlock;
+    const int64_t groups = ceil_div(n, kRowsPerWord);
+    const int64_t ng = min64(kEncGroupsPerBlock, groups - g0);
+    uint32_t* dst = codes + g0 * m;
+    for (int64_t e = threadIdx.x; e < ng * m; e += blockDim.x) dst[e] = stage[e];
+}
+
+__global__ void pack_kernel(const uint8_t* __restrict__ flat, int64_t n, int m,
+                            uint32_t* __restrict__ codes) {
+    int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = ceil_div(n, kRowsPerWord) * m;
+    if (w >= total) return;
+    int64_t g = w / m;
+    int c = (int)(w - g * m);
+    uint32_t word = 0;
+    for (int r = 0; r < kRowsPerWord; ++r) {
+        int64_t i = g * kRowsPerWord + r;
+        if (i < n) word |= (uint32_t)(flat[i * m + c] & 0xF) << (4 * r);
+    }
+    codes[w] = word;
+}
+
+__global__ void unpack_kernel(const uint32_t* __restrict__ codes, int64_t n, int m,
+                              uint8_t* __restrict__ flat) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * m) return;
+    int64_t i = e / m;
+    int c = (int)(e - i * m);
+    flat[e] = (uint8_t)((codes[(i >> 3) * m + c] >> (4 * (i & 7))) & 0xF);
+}
+
+}  // namespace
+
+cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,
+                          uint32_t* codes, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const int L = j / m;
+    size_t smem = (size_t)j * kK * sizeof(float) + (size_t)kEncGroupsPerBlock * m * sizeof(uint32_t);
+    bool vec = (L % 4 == 0) && (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+    int64_t blocks = ceil_div(n, kEncRowsPerBlock);
+    if (vec) {
+        cudaFuncSetAttribute(encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        encode_kernel<true><<<(unsigned)blocks, kEncThreads, smem, s>>>(X, n, j, ldx, C, m, codes);
+    } else {
+        cudaFuncSetAttribute(encode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        encode_kernel<false><<<(unsigned)blocks, kEncThreads, smem, s>>>(X, n, j, ldx, C, m, codes);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack(const uint8_t* flat, int64_t n, int m, uint32_t* codes, cudaStream_t s) {
+    int64_t total = ceil_div(n, kRowsPerWord) * m;
+    if (total == 0) return cudaSuccess;
+    pack_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(flat, n, m, codes);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(const uint32_t* codes, int64_t n, int m, uint8_t* flat, cudaStream_t s) {
+    int64_t total = n * m;
+    if (total == 0) return cudaSuccess;
+    unpack_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, s>>>(codes, n, m, flat);
+    return cudaGetLastError();
+}
+
+}  // namespace bolt

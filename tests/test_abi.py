@@ -1,0 +1,80 @@
+"""C-ABI library checks that need no GPU: the in-tree libbolt.so loads, exports
+every symbol include/bolt.h declares, and rejects bad arguments on the host
+before touching a device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "bolt.h")
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(bolt_[a-z0-9_]+)\s*\(", txt)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1706_10283_b200 import _lib, build
+    build.build()
+    return _lib.load()
+
+
+def test_header_symbols_exported(lib):
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    from paper_1706_10283_b200 import _lib
+    for s in syms:
+        assert hasattr(lib, s), f"{s} declared in bolt.h but not exported"
+        assert s in _lib.SIGNATURES, f"{s} has no ctypes signature in the binding"
+    # nothing exported that the header does not declare
+    out = os.popen(f"nm -D --defined-only {_lib.LIB_PATH}").read()
+    exported = set(re.findall(r"\bT (bolt_\w+)", out))
+    assert exported == set(syms), exported ^ set(syms)
+
+
+def test_version_and_words(lib):
+    assert b"sm_100a" in lib.bolt_version()
+    assert lib.bolt_codes_words(0, 16) == 0
+    assert lib.bolt_codes_words(1, 16) == 16
+    assert lib.bolt_codes_words(8, 16) == 16
+    assert lib.bolt_codes_words(9, 3) == 6
+    assert lib.bolt_codes_words(10, 0) == -1
+    assert lib.bolt_codes_words(10, 65) == -1
+
+
+def test_host_validation(lib):
+    from paper_1706_10283_b200._lib import STATUS
+    E_SHAPE, E_RANGE, E_NULL = 2, 3, 1
+    # shape errors are reported before any device access
+    assert lib.bolt_encode(None, 10, 32, 32, None, 0, None, None) == E_SHAPE
+    assert "outside 1..64" in lib.bolt_last_error().decode()
+    assert lib.bolt_encode(None, 10, 30, 30, None, 8, None, None) == E_SHAPE
+    assert "not divisible" in lib.bolt_last_error().decode()
+    assert lib.bolt_encode(None, 10, 32, 16, None, 8, None, None) == E_SHAPE
+    assert lib.bolt_encode(None, 10, 32, 32, None, 8, None, None) == E_NULL
+    assert lib.bolt_encode(None, 0, 32, 32, None, 8, None, None) == 0  # empty is a no-op
+    assert lib.bolt_quantize_luts(None, 4, 8, ctypes.c_float(0.0), None, None, None) == E_RANGE
+    assert lib.bolt_scan(None, 10, 8, None, 4, None, 2, None) == E_NULL
+    assert lib.bolt_topk_ex(None, 10, 8, None, 4, 0, 0, 0, None, None, 0, 0, None) == E_NULL
+    k = ctypes.c_void_p(16)
+    assert lib.bolt_topk_ex(k, 10, 8, k, 4, 0, 0, 0, None, None, 0, 0, None) == E_SHAPE
+    assert lib.bolt_topk_ex(k, 10, 8, k, 4, 129, 0, 0, None, None, 0, 0, None) == E_SHAPE
+    assert lib.bolt_topk_ex(k, 10, 8, k, 4, 10, 2, 0, None, None, 0, 0, None) == E_RANGE
+    assert lib.bolt_topk_ex(k, 10, 8, k, 4, 10, 0, 0, None, None, 0, 7, None) == E_RANGE
+    assert lib.bolt_topk_ex(k, 10, 8, k, 4, 10, 0, 1 << 48, None, None, 0, 0, None) == E_RANGE
+    assert lib.bolt_topk_merge(None, 100, 4, 100, None, None) == E_SHAPE
+    assert set(STATUS) == set(range(8))
+
+
+def test_workspace_sizing_host(lib):
+    # the plan is a pure function of the shapes (and SM count): parts * nq * k * 8 bytes
+    for n, m, nq, k in [(10, 8, 4, 10), (1_000_000, 16, 10_000, 10), (10**8, 16, 1, 100)]:
+        ws = lib.bolt_topk_workspace_bytes_ex(n, m, nq, k, 1)
+        assert ws % (nq * k * 8) == 0
+        parts = ws // (nq * k * 8)
+        assert parts == 0 or 2 <= parts <= 8192 // k

@@ -1,0 +1,290 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle on
+identical seeded inputs.  Contract (SURVEY 8(c) / BASELINE.json north_star):
+  * scan u16 sums, top-k keys (values, indices, order, lower-index ties), merge,
+    pack/unpack: bit-exact;
+  * fp32 tables: |gpu - oracle| <= 1e-4 * max|D(q)| per query;
+  * quantized tables and codes: exact except near-ties (|t - rint(t)| < 1e-3, or
+    relative centroid-distance gap < 1e-5), counted, cap 0.01 %;
+  * dequant: |gpu - oracle| <= 2^-21 (|acc/a| + |sum b|).
+"""
+import numpy as np
+import pytest
+import torch
+
+from synth import generators as G
+
+pytestmark = pytest.mark.gpu
+
+NEAR_TIE_CAP = 1e-4  # 0.01 %
+
+
+@pytest.fixture(scope="module")
+def bolt():
+    import paper_1706_10283_b200 as bolt
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    bolt._lib.load()
+    return bolt
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def pack_on_gpu(bolt, flat):
+    return bolt.pack_codes(dev(flat.astype(np.uint8)))
+
+
+# --------------------------------------------------------------------- layout
+@pytest.mark.parametrize("n,m", [(1, 1), (7, 3), (8, 16), (9, 16), (1001, 8), (4097, 64)])
+def test_pack_unpack_layout_v1(bolt, orc, n, m):
+    flat = G.random_codes(n, m, n * 7 + m)
+    words = host(pack_on_gpu(bolt, flat))
+    assert words.size == bolt.codes_words(n, m)
+    np.testing.assert_array_equal(orc.unpack_v1(words, n, m), flat)      # O12 reads GPU layout
+    np.testing.assert_array_equal(host(bolt.unpack_codes(dev(words), n, m)), flat)
+
+
+# --------------------------------------------------------------------- encode
+def _encode_check(bolt, orc, X, C):
+    n = X.shape[0]
+    m = C.shape[0]
+    words = host(bolt.encode(dev(X), dev(C)))
+    got = orc.unpack_v1(words, n, m)
+    ref, gap = orc.encode(X, C, with_gap=True)
+    diff = got != ref
+    exempt = diff & (gap < 1e-5)
+    assert (diff == exempt).all(), f"{(diff & ~exempt).sum()} non-tie code mismatches"
+    assert exempt.sum() <= NEAR_TIE_CAP * diff.size + 1e-9, f"near-ties {exempt.sum()} over cap"
+    return exempt.sum()
+
+
+@pytest.mark.parametrize("n,m,L", [(1, 1, 1), (9, 2, 3), (513, 4, 4), (1000, 8, 4), (4099, 16, 8),
+                                   (777, 32, 16), (300, 64, 2), (100, 5, 7)])
+def test_encode_random(bolt, orc, n, m, L):
+    X = G.random_floats((n, m * L), 1000 + n)
+    C = G.random_floats((m, 16, L), 2000 + m)
+    _encode_check(bolt, orc, X, C)
+
+
+def test_encode_centroid_identity(bolt, orc):
+    m, L = 16, 8
+    C = G.random_floats((m, 16, L), 5)
+    idx = np.random.default_rng(0).integers(0, 16, (1000, m))
+    X = np.ascontiguousarray(np.concatenate([C[c][idx[:, c]] for c in range(m)], axis=1))
+    got = orc.unpack_v1(host(bolt.encode(dev(X), dev(C))), 1000, m)
+    np.testing.assert_array_equal(got, idx)
+
+
+# ------------------------------------------------------------------------ LUT
+@pytest.mark.parametrize("metric", [0, 1])
+@pytest.mark.parametrize("nq,m,L", [(1, 1, 1), (16, 8, 4), (33, 16, 8), (7, 32, 16), (5, 64, 3)])
+def test_luts(bolt, orc, metric, nq, m, L):
+    Q = G.random_floats((nq, m * L), 3000 + nq, scale=3.0)
+    C = G.random_floats((m, 16, L), 4000 + m)
+    ref = orc.luts(Q, C, metric)
+    d64 = host(bolt.build_luts(dev(Q), dev(C), metric, f64=True))
+    np.testing.assert_array_equal(d64, ref)       # same fp64 operations in the same order
+    d32 = host(bolt.build_luts(dev(Q), dev(C), metric))
+    tol = 1e-4 * np.abs(ref).reshape(nq, -1).max(axis=1)
+    assert (np.abs(d32 - ref).reshape(nq, -1) <= tol[:, None]).all()
+
+
+def _quant_params(m, seed, lo=-1.0, hi=1.0):
+    rng = np.random.default_rng(seed)
+    return np.float32(rng.uniform(3, 40)), rng.uniform(lo, hi, m).astype(np.float32)
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+def test_quantize_fused_and_standalone(bolt, orc, metric):
+    nq, m, L = 64, 16, 8
+    Q = G.random_floats((nq, m * L), 11)
+    C = G.random_floats((m, 16, L), 12)
+    a, b = _quant_params(m, 13, *((-1, 5) if metric == 0 else (-3, 0)))
+    D = orc.luts(Q, C, metric)
+    ref, t = orc.quantize(D, a, b, with_t=True)
+    got, f32 = bolt.build_quantized_luts(dev(Q), dev(C), metric, float(a), dev(b), return_f32=True)
+    got = host(got)
+    diff = got != ref
+    near = np.abs(t - np.rint(t)) < 1e-3
+    assert (diff <= near).all()
+    assert diff.sum() <= NEAR_TIE_CAP * diff.size
+    assert (0 < ref).any() and (ref < 255).any() and (ref == 0).any()
+    # standalone quantize of the GPU fp32 tables: oracle promotes the same fp32 values
+    d32 = host(f32)
+    ref2 = orc.quantize(d32.astype(np.float64), a, b)
+    np.testing.assert_array_equal(host(bolt.quantize_luts(dev(d32), float(a), dev(b))), ref2)
+
+
+# ----------------------------------------------------------------------- scan
+SCAN_SHAPES = [(1, 1, 1), (7, 2, 3), (8, 16, 1), (9, 16, 2), (1000, 8, 16), (4097, 16, 9),
+               (1234, 17, 5), (513, 32, 8), (333, 33, 4), (2049, 64, 17), (100, 3, 8), (64, 4, 1)]
+
+
+@pytest.mark.parametrize("n,m,nq", SCAN_SHAPES)
+def test_scan_bitexact(bolt, orc, n, m, nq):
+    flat = G.random_codes(n, m, n + 17 * m)
+    ql = G.random_qluts(nq, m, nq + 31 * m)
+    ref = orc.scan(flat, ql)
+    got = host(bolt.scan(pack_on_gpu(bolt, flat), n, dev(ql)))
+    np.testing.assert_array_equal(got, ref)
+
+
+def test_scan_extremes(bolt, orc):
+    n, m, nq = 999, 64, 3
+    flat = G.random_codes(n, m, 1)
+    ql = np.full((nq, m, 16), 255, np.uint8)
+    ql[1] = 0
+    ql[2, :, 15] = 255
+    ql[2, :, :15] = 128
+    got = host(bolt.scan(pack_on_gpu(bolt, flat), n, dev(ql)))
+    np.testing.assert_array_equal(got, orc.scan(flat, ql))
+    assert got[:, 0].max() == 255 * 64
+
+
+def test_scan_dequant(bolt, orc):
+    n, m, nq = 2001, 32, 40
+    flat = G.random_codes(n, m, 2)
+    ql = G.random_qluts(nq, m, 3)
+    a, b = _quant_params(m, 4, -2, 1)
+    acc = orc.scan(flat, ql)
+    ref = orc.dequant(acc, a, b)
+    bsum = float(np.sum(b.astype(np.float64)))
+    got = host(bolt.scan_dequant(pack_on_gpu(bolt, flat), n, dev(ql), float(a), np.float32(bsum)))
+    tol = 2.0 ** -21 * (np.abs(acc / np.float64(a)) + abs(bsum))
+    assert (np.abs(got - ref) <= tol).all()
+
+
+# ---------------------------------------------------------------------- top-k
+TOPK_CASES = [
+    # n, m, nq, k, lut_hi (small -> many ties), index_base
+    (1, 1, 1, 1, 256, 0),
+    (5, 4, 3, 10, 256, 0),            # k > n: padding
+    (100, 8, 16, 10, 4, 0),
+    (1000, 16, 9, 1, 256, 5),
+    (4097, 16, 33, 10, 16, 0),
+    (2500, 8, 20, 32, 8, 123456),
+    (3000, 32, 7, 33, 256, 0),
+    (5000, 16, 5, 100, 32, 0),
+    (20000, 16, 8, 128, 256, 2**40),
+    (65537, 16, 3, 10, 8, 0),
+    (10000, 64, 4, 64, 256, 0),
+]
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+@pytest.mark.parametrize("n,m,nq,k,hi,base", TOPK_CASES)
+def test_topk_prmt_bitexact(bolt, orc, metric, n, m, nq, k, hi, base):
+    flat = G.random_codes(n, m, n + m + k)
+    ql = G.random_qluts(nq, m, nq + k, hi=hi)
+    ref = orc.topk(flat, ql, k, metric, index_base=base)
+    got = host(bolt.topk(pack_on_gpu(bolt, flat), n, dev(ql), k, metric, index_base=base,
+                         variant=bolt.VARIANT_PRMT))
+    np.testing.assert_array_equal(got, ref)
+
+
+def test_topk_constant_tables_all_ties(bolt, orc):
+    """Every distance equal: the answer is the k lowest indices."""
+    n, m, nq, k = 3001, 16, 4, 50
+    flat = G.random_codes(n, m, 9)
+    ql = np.full((nq, m, 16), 7, np.uint8)
+    for metric in (0, 1):
+        got = host(bolt.topk(pack_on_gpu(bolt, flat), n, dev(ql), k, metric, variant=bolt.VARIANT_PRMT))
+        np.testing.assert_array_equal(got, orc.topk(flat, ql, k, metric))
+        v, idx = bolt.keys_split(dev(got), metric)
+        np.testing.assert_array_equal(host(idx)[0], np.arange(k))
+
+
+def test_merge_and_split(bolt, orc):
+    n, m, nq, k = 6000, 8, 12, 20
+    flat = G.random_codes(n, m, 21)
+    ql = G.random_qluts(nq, m, 22, hi=16)
+    bounds = [0, 8, 1600, 1608, 4000, 6000]
+    parts = []
+    for lo, hi_ in zip(bounds[:-1], bounds[1:]):
+        codes = pack_on_gpu(bolt, flat[lo:hi_])
+        parts.append(bolt.topk(codes, hi_ - lo, dev(ql), k, 0, index_base=lo))
+    merged = host(bolt.topk_merge(torch.stack(parts)))
+    np.testing.assert_array_equal(merged, orc.topk(flat, ql, k, 0))
+    np.testing.assert_array_equal(merged, orc.merge(np.stack([host(p) for p in parts])))
+    for metric in (0, 1):
+        keys = orc.topk(flat, ql, k, metric)
+        v, idx = bolt.keys_split(dev(keys), metric)
+        rv, ridx = orc.keys_split(keys, metric)
+        np.testing.assert_array_equal(host(v), rv)
+        np.testing.assert_array_equal(host(idx), ridx)
+
+
+# ------------------------------------------------------------ configs (c1)
+@pytest.fixture(scope="module")
+def c1_model(orc):
+    cfg = G.CONFIGS["c1"]
+    X = G.database(cfg)
+    init = G.kmeans_init_all(cfg, len(X))
+    C = orc.fit(X, cfg.m, init, cfg.kmeans_iters)
+    calib = G.calibration(cfg, X)
+    params = {mt: orc.fit_quantizer(calib, C, mt) for mt in cfg.metrics}
+    return cfg, X, C, params
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+def test_c1_end_to_end(bolt, orc, c1_model, metric):
+    """BASELINE c1: encode, fused tables, full N x Q u16 output, top-10."""
+    cfg, X, C, params = c1_model
+    a, b, _ = params[metric]
+    Q = G.queries(cfg)
+    codes = bolt.encode(dev(X), dev(C))
+    _encode_check(bolt, orc, X, C)
+    gcodes = orc.unpack_v1(host(codes), cfg.n, cfg.m)
+    D = orc.luts(Q, C, metric)
+    ref_q, t = orc.quantize(D, a, b, with_t=True)
+    ql = host(bolt.build_quantized_luts(dev(Q), dev(C), metric, float(a), dev(b)))
+    assert ((ql != ref_q) <= (np.abs(t - np.rint(t)) < 1e-3)).all()
+    out = host(bolt.scan(codes, cfg.n, dev(ql)))
+    np.testing.assert_array_equal(out, orc.scan(gcodes, ql))
+    keys = host(bolt.topk(codes, cfg.n, dev(ql), 10, metric))
+    np.testing.assert_array_equal(keys, orc.topk(gcodes, ql, 10, metric))
+
+
+def test_search_host_matches_device_path(bolt, orc, c1_model):
+    cfg, X, C, params = c1_model
+    a, b, _ = params[0]
+    Q = G.queries(cfg)
+    hs = bolt.HostSearch(cfg.n, cfg.j, cfg.m, cfg.nq, 10)
+    keys_h = torch.empty((cfg.nq, 10), dtype=torch.uint64).pin_memory()
+    hs(torch.from_numpy(X).pin_memory(), torch.from_numpy(Q).pin_memory(), dev(C), 0, float(a), dev(b), keys_h)
+    torch.cuda.synchronize()
+    codes = bolt.encode(dev(X), dev(C))
+    ql = bolt.build_quantized_luts(dev(Q), dev(C), 0, float(a), dev(b))
+    np.testing.assert_array_equal(keys_h.numpy(), host(bolt.topk(codes, cfg.n, ql, 10, 0)))
+
+
+# ----------------------------------------------------- c2 at full size (sampled)
+@pytest.mark.slow
+def test_c2_full_size_sampled(bolt, orc):
+    """BASELINE c2 (N=1M, J=128, M=16, Q=10k, top-10) in the launch configuration
+    bench.py times; the oracle checks 16 sampled queries over the full GPU code
+    set (read with O12) and 20k sampled rows of the encoder."""
+    cfg = G.CONFIGS["c2"]
+    X = G.database(cfg)
+    train = G.training(cfg, 20_000)
+    init = G.kmeans_init_all(cfg, len(train))
+    C = orc.fit(train, cfg.m, init, 4)
+    a, b, _ = orc.fit_quantizer(G.calibration(cfg, train)[:200], C, 0)
+    Q = G.queries(cfg)
+    Xd, Qd = dev(X), dev(Q)
+    codes = bolt.encode(Xd, dev(C))
+    ql = bolt.build_quantized_luts(Qd, dev(C), 0, float(a), dev(b))
+    keys = host(bolt.topk(codes, cfg.n, ql, cfg.k, 0))
+    gcodes = orc.unpack_v1(host(codes), cfg.n, cfg.m)
+    rows = np.random.default_rng(1).choice(cfg.n, 20_000, replace=False)
+    ref_codes, gap = orc.encode(X[rows], C, with_gap=True)
+    d = gcodes[rows] != ref_codes
+    assert (d <= (gap < 1e-5)).all() and d.sum() <= NEAR_TIE_CAP * d.size
+    qs = np.random.default_rng(2).choice(cfg.nq, 16, replace=False)
+    qlh = host(ql)
+    np.testing.assert_array_equal(keys[qs], orc.topk(gcodes, qlh[qs], cfg.k, 0))
