@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Bolt hot-path benchmark (BASELINE.json metric: billion query x code
+distances / s at M=16, J=128; % of roofline).
+
+One step = the whole §8(a) path over one batch of BASELINE c2 (synthetic
+SIFT1M-like: N=1,000,000 x J=128 fp32 database per GPU, Q=10,000 queries,
+M=16, squared L2, top-10):
+    encode(X)  ->  fused fp64 LUT build + u8 quantize(Q)  ->  scan + top-10
+    [N > 1: NCCL all-gather of the [Q][10] u64 keys + merge]
+value = distances (all ranks) / step time, inputs resident in HBM.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--variant auto|prmt|tc]
+    python bench.py --impl reference ...      # the fp64 CPU oracle arm
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Timing: CUDA events on the launching stream, W untimed warm-up steps, K timed
+steps between barrier + synchronize, max over ranks.  The 512 MB fp32 database
+that every step streams through the encoder exceeds the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from synth import generators as G  # noqa: E402
+
+METRIC = "Bolt scan: billion query×code distances/sec (M=16, J=128); % of roofline"
+UNIT = "Gdist/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2")
+    p.add_argument("--variant", default="auto", choices=["auto", "prmt", "tc"])
+    p.add_argument("--n", type=int, default=0, help="override rows per GPU (debug)")
+    p.add_argument("--nq", type=int, default=0, help="override queries (debug)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period: float = 0.02):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - no NVML
+            self.nv = None
+            self.err = str(e)
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                fn = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    self.nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                r = fn(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0}, "fallback"
+
+
+def profile_traffic(variant: str):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(variant)
+    return None
+
+
+# ------------------------------------------------------------- workload
+def workload(args, rank):
+    cfg = G.CONFIGS[args.config]
+    n = args.n or cfg.n
+    nq = args.nq or cfg.nq
+    return cfg, n, nq
+
+
+def cpu_baseline_sample(cfg, X, Q, C, a, b, metric, k, budget_s=20.0):
+    """The fp64 oracle, as it stands, on the host cores: encode of the full
+    database shard, tables of all queries, and the scan + top-k for a sample
+    of queries over the full database; the scan time is scaled to all
+    queries.  Returns (distances/s, threads, description)."""
+    from oracle import oracle
+    n, nq = len(X), len(Q)
+    threads = oracle.num_threads()
+    t0 = time.perf_counter()
+    flat = oracle.encode(X, C)
+    t_enc = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ql = oracle.quantize(oracle.luts(Q, C, metric), a, b)
+    t_lut = time.perf_counter() - t0
+    # size the scan sample to the remaining budget (at least 8 queries)
+    t0 = time.perf_counter()
+    oracle.topk(flat, ql[:8], k, metric)
+    t8 = time.perf_counter() - t0
+    qs = int(max(8, min(nq, 8 * max(1.0, (budget_s - t_enc - t_lut - t8) / max(t8, 1e-3)))))
+    qs = min(qs, 1024)
+    t0 = time.perf_counter()
+    oracle.topk(flat, ql[:qs], k, metric)
+    t_scan = time.perf_counter() - t0
+    t_full = t_enc + t_lut + t_scan * (nq / qs)
+    desc = (f"oracle encode of all {n} rows ({t_enc:.2f} s) + fp64 tables of all {nq} queries "
+            f"({t_lut:.2f} s) + scan/top-{k} of {qs} queries over all rows ({t_scan:.2f} s), "
+            f"scan scaled x{nq / qs:.1f} to {nq} queries")
+    return n * nq / t_full / 1e9, threads, desc
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1706_10283_b200 as bolt
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg, n, nq = workload(args, rank)
+    metric = cfg.metrics[0]
+    k = cfg.k
+    variant = {"auto": bolt.VARIANT_AUTO, "prmt": bolt.VARIANT_PRMT, "tc": bolt.VARIANT_TC}[args.variant]
+
+    # --- inputs (seeded, synthetic); rank r holds database rows [r*n, (r+1)*n)
+    X = G.database(cfg, n, start=rank * n)
+    Q = G.queries(cfg, nq)
+    train = G.training(cfg)
+    init = G.kmeans_init_all(cfg, len(train))
+    calib = G.calibration(cfg, train)
+    Xd = torch.from_numpy(X).to(dev)
+    Qd = torch.from_numpy(Q).to(dev)
+
+    # --- offline fit on the GPU (not timed): k-means + LUT quantizer
+    model = bolt.BoltModel.fit(torch.from_numpy(train).to(dev), cfg.m, torch.from_numpy(init).to(dev),
+                               torch.from_numpy(calib).to(dev), metric, iters=cfg.kmeans_iters)
+    del train
+
+    words = bolt.codes_words(n, cfg.m)
+    codes = torch.empty(words, dtype=torch.uint32, device=dev)
+    ql = torch.empty((nq, cfg.m, 16), dtype=torch.uint8, device=dev)
+    keys = torch.empty((nq, k), dtype=torch.uint64, device=dev)
+    wsb = bolt.topk_workspace_bytes(n, cfg.m, nq, k, variant)
+    ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
+    gathered = torch.empty((world, nq, k), dtype=torch.uint64, device=dev) if world > 1 else None
+    final = torch.empty((nq, k), dtype=torch.uint64, device=dev) if world > 1 else keys
+    stream = torch.cuda.current_stream(dev)
+    ev_scan = []
+
+    def step(timed: bool):
+        bolt.encode(Xd, model.C, out=codes)
+        bolt.build_quantized_luts(Qd, model.C, metric, model.a, model.b, out=ql)
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        bolt.topk(codes, n, ql, k, metric, index_base=rank * n, variant=variant, out=keys, workspace=ws)
+        if timed:
+            e1.record(stream)
+            ev_scan.append((e0, e1))
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, keys)
+            bolt.topk_merge(gathered, out=final)
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
+                       int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local]))
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with clk:
+        t_start.record(stream)
+        for _ in range(args.steps):
+            step(True)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_local = t_start.elapsed_time(t_end)
+    scan_ms = sum(a.elapsed_time(b) for a, b in ev_scan) / len(ev_scan)
+    ms = ms_local
+    if world > 1:
+        t = torch.tensor([ms_local, scan_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, scan_ms = float(t[0]), float(t[1])
+    ms_step = ms / args.steps
+    dists = world * n * nq
+    value = dists / (ms_step * 1e-3) / 1e9
+
+    # --- e2e through the public host-buffer API (H2D of X, Q inside the timed region)
+    e2e = None
+    if args.e2e_steps > 0:
+        hs = bolt.HostSearch(n, cfg.j, cfg.m, nq, k, device=dev)
+        Xh = torch.from_numpy(X).pin_memory()
+        Qh = torch.from_numpy(Q).pin_memory()
+        kh = torch.empty((nq, k), dtype=torch.uint64).pin_memory()
+        kd = torch.empty((nq, k), dtype=torch.uint64, device=dev)
+
+        def e2e_step():
+            hs(Xh, Qh, model.C, metric, model.a, model.b, kh)
+            if world > 1:
+                kd.copy_(kh, non_blocking=True)
+                dist.all_gather_into_tensor(gathered, kd)
+                bolt.topk_merge(gathered, out=final)
+                kh.copy_(final, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a0.elapsed_time(a1) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t[0])
+        e2e = {"value": round(dists / (e_ms * 1e-3) / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": int(X.nbytes + Q.nbytes),
+               "d2h_bytes_per_step": int(nq * k * 8), "ms_per_step": round(e_ms, 3),
+               "api": "bolt_search_host (pinned host X, Q -> keys)"}
+
+    # --- roofline of the dominant kernel (scan + fused top-k)
+    peaks, peak_src = measured_peaks()
+    used_variant, parts = bolt.topk_plan(n, cfg.m, nq, k, variant)
+    roof = roofline(used_variant, n, cfg.m, nq, scan_ms, peaks, peak_src, clk.summary())
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded SIFT1M-like Gaussian mixture, SURVEY 8(d) c2 recipe)",
+            "config": {"workload": f"{args.config}: N={n} rows/GPU x J={cfg.j} fp32, M={cfg.m} (4-bit codes), "
+                                   f"Q={nq}, squared L2, top-{k}; step = encode + fp64 LUT build/quantize "
+                                   f"+ scan/top-k" + (" + NCCL all-gather + merge" if world > 1 else ""),
+                       "n_per_gpu": n, "nq": nq, "m": cfg.m, "j": cfg.j, "k": k,
+                       "variant": used_variant, "scan_parts": parts,
+                       "l2": "inputs > L2: the 512 MB fp32 database is streamed by the encoder every step",
+                       "parallelism": f"row-sharded dp{world}"},
+            "roofline": roof,
+            "e2e": e2e,
+            "gpu_launches": args.steps * (3 + (1 if parts > 1 else 0) + (1 if world > 1 else 0)),
+            "clocks": clk.summary(),
+            "scan_ms": round(scan_ms, 4),
+        }
+        if not args.no_cpu_baseline and world == 1:
+            v, cores, desc = cpu_baseline_sample(cfg, X, Q, model.C.cpu().numpy(), np.float32(model.a),
+                                                 model.b.cpu().numpy(), metric, k)
+            out["cpu_baseline"] = {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
+                                   "sample": desc}
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def roofline(variant, n, m, nq, scan_ms, peaks, peak_src, clocks):
+    """Dominant kernel = the scan with fused top-k (bolt_topk; includes the tiny
+    split-N partial merge).  PRMT: integer-ALU bound, algorithmic work
+    2*M int ops per distance (M lookups + M adds); peak = 148 SM
+    x 128 int lanes/clk (alu + fma pipes, 1 warp-instruction/clk/SMSP issue)
+    x max SM clock (B300_MICROARCH.md pipe rates).  TC: tensor
+    bound, one-hot contraction executes 2*16*M int8 ops per distance; peak =
+    dense int8 = 2 x measured bf16 (nominal 4.5 / 2.25 PF ratio)."""
+    t = scan_ms * 1e-3
+    dists = n * nq
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    if variant == "tc":
+        ops = 2.0 * 16 * m * dists
+        peak = 2.0 * peaks["bf16_tflops"] * 1e12
+        achieved = ops / t
+        return {"bound": "tensor", "achieved": round(achieved / 1e12, 2), "peak": round(peak / 1e12, 2),
+                "unit": "TOP/s", "frac": round(achieved / peak, 4), "traffic": profile_traffic("tc"),
+                "peak_source": f"int8 dense = 2 x {peak_src} bf16 ({peaks['bf16_tflops']} TFLOP/s)",
+                "kernel": "bolt_topk (tcgen05 scan + top-k)", "kernel_ms": round(scan_ms, 4)}
+    ops = 2.0 * m * dists
+    peak = 148 * 128 * sm_mhz * 1e6
+    achieved = ops / t
+    return {"bound": "alu", "achieved": round(achieved / 1e12, 3), "peak": round(peak / 1e12, 3),
+            "unit": "Tops/s", "frac": round(achieved / peak, 4), "traffic": profile_traffic("prmt"),
+            "peak_source": f"148 SM x 128 int lanes/clk x {sm_mhz:.0f} MHz ({peak_src} sm_max_mhz); DESIGN.md",
+            "kernel": "bolt_topk (PRMT scan + fused top-k)", "kernel_ms": round(scan_ms, 4),
+            "hbm_view": {"algorithmic_bytes": n * m // 2 + nq * m * 16 + nq * 10 * 8,
+                         "gbs": round((n * m // 2 + nq * m * 16) / t / 1e9, 1)}}
+
+
+# ------------------------------------------------------------- reference
+def run_reference(args):
+    """The fp64 CPU oracle as it stands, on the host cores (rank 0 only)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle
+    cfg, n, nq = workload(args, rank)
+    metric, k = cfg.metrics[0], cfg.k
+    X = G.database(cfg, n)
+    Q = G.queries(cfg, nq)
+    train = G.training(cfg, 20_000)
+    C = oracle.fit(train, cfg.m, G.kmeans_init_all(cfg, len(train)), cfg.kmeans_iters)
+    a, b, _ = oracle.fit_quantizer(G.calibration(cfg, train)[:200], C, metric)
+    budget = max(5.0, 120.0 / max(1, args.steps + args.warmup))
+    vals = []
+    desc = cores = None
+    for i in range(args.warmup + args.steps):
+        v, cores, desc = cpu_baseline_sample(cfg, X, Q, C, a, b, metric, k, budget_s=budget)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.mean(vals)
+    ms = world * n * nq / (value * 1e9) * 1e3
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64/int64", "data": "synthetic",
+           "config": {"workload": f"{args.config}: N={n} x J={cfg.j}, M={cfg.m}, Q={nq}, top-{k} (fp64 CPU oracle)",
+                      "n_per_gpu": n, "nq": nq},
+           "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": desc},
+           "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

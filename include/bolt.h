@@ -152,6 +152,11 @@ BOLT_API size_t bolt_topk_workspace_bytes(int64_t n, int m, int64_t nq, int k);
 BOLT_API bolt_status bolt_topk(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts, int64_t nq,
                       int k, bolt_metric metric, int64_t index_base, uint64_t* out_keys, void* ws,
                       size_t ws_bytes, bolt_stream_t stream);
+/* The plan bolt_topk_ex will use for these shapes (host): the resolved
+ * variant (BOLT_VARIANT_PRMT / BOLT_VARIANT_TC) and the number of row
+ * partitions whose partial lists are merged (1 = no merge). */
+BOLT_API bolt_status bolt_topk_plan(int64_t n, int m, int64_t nq, int k, int variant,
+                                    int* resolved_variant, int* parts);
 /* As bolt_topk with an explicit scan variant (tests, benchmarks). */
 BOLT_API size_t bolt_topk_workspace_bytes_ex(int64_t n, int m, int64_t nq, int k, int variant);
 BOLT_API bolt_status bolt_topk_ex(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts,
@@ -160,7 +165,7 @@ BOLT_API bolt_status bolt_topk_ex(const uint32_t* codes, int64_t n, int m, const
                          bolt_stream_t stream);
 
 /* Merge w sorted key lists [w][nq][k] (indices already global) into the k
- * smallest keys per query [nq][k]; w*k <= 8192.  Equals bolt_topk over the
+ * smallest keys per query [nq][k]; 1 <= w <= 16384, 1 <= k <= 128.  Equals bolt_topk over the
  * union of the shards bit for bit. */
 BOLT_API bolt_status bolt_topk_merge(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out_keys,
                             bolt_stream_t stream);

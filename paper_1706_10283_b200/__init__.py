@@ -156,6 +156,14 @@ def topk_workspace_bytes(n: int, m: int, nq: int, k: int, variant: int = VARIANT
     return int(_lib.load().bolt_topk_workspace_bytes_ex(n, m, nq, k, variant))
 
 
+def topk_plan(n: int, m: int, nq: int, k: int, variant: int = VARIANT_AUTO):
+    """-> (resolved variant name 'prmt' | 'tc', number of merged row partitions)."""
+    import ctypes
+    v, p = ctypes.c_int(0), ctypes.c_int(0)
+    _lib.call("bolt_topk_plan", n, m, nq, k, variant, ctypes.byref(v), ctypes.byref(p))
+    return ("prmt" if v.value == VARIANT_PRMT else "tc"), p.value
+
+
 def topk(codes: torch.Tensor, n: int, qluts: torch.Tensor, k: int, metric, index_base: int = 0,
          variant: int = VARIANT_AUTO, out: torch.Tensor | None = None,
          workspace: torch.Tensor | None = None) -> torch.Tensor:

@@ -33,6 +33,7 @@ SIGNATURES = {
     "bolt_scan_dequant": ([_P, _I64, _I32, _P, _I64, _F32, _F32, _P, _I64, _P], _I32),
     "bolt_topk_workspace_bytes": ([_I64, _I32, _I64, _I32], _SZ),
     "bolt_topk": ([_P, _I64, _I32, _P, _I64, _I32, _I32, _I64, _P, _P, _SZ, _P], _I32),
+    "bolt_topk_plan": ([_I64, _I32, _I64, _I32, _I32, _P, _P], _I32),
     "bolt_topk_workspace_bytes_ex": ([_I64, _I32, _I64, _I32, _I32], _SZ),
     "bolt_topk_ex": ([_P, _I64, _I32, _P, _I64, _I32, _I32, _I64, _P, _P, _SZ, _I32, _P], _I32),
     "bolt_topk_merge": ([_P, _I32, _I64, _I32, _P, _P], _I32),

@@ -250,6 +250,17 @@ size_t bolt_topk_workspace_bytes_ex(int64_t n, int m, int64_t nq, int k, int var
     return topk_plan(n, m, nq, k, variant, sms_or_default()).ws;
 }
 
+bolt_status bolt_topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int* resolved_variant,
+                           int* parts) {
+    TRY(check_m(m));
+    if (n < 0 || nq < 0 || k < 1 || k > kMaxK) return fail(BOLT_E_SHAPE, "bad n/nq/k");
+    if (variant < BOLT_VARIANT_AUTO || variant > BOLT_VARIANT_TC) return fail(BOLT_E_RANGE, "variant %d", variant);
+    TopkPlan p = topk_plan(n, m, nq, k, variant, sms_or_default());
+    if (resolved_variant) *resolved_variant = p.variant;
+    if (parts) *parts = p.parts;
+    return BOLT_OK;
+}
+
 size_t bolt_topk_workspace_bytes(int64_t n, int m, int64_t nq, int k) {
     return bolt_topk_workspace_bytes_ex(n, m, nq, k, BOLT_VARIANT_AUTO);
 }
@@ -280,8 +291,8 @@ bolt_status bolt_topk_ex(const uint32_t* codes, int64_t n, int m, const uint8_t*
     ScanArgs a{codes, n, ceil_div(n, 8), m, qluts, nq};
     uint64_t* parts_out = p.parts > 1 ? static_cast<uint64_t*>(ws) : out_keys;
     cudaError_t e = p.variant == BOLT_VARIANT_TC
-                        ? launch_topk_tc(a, k, metric, index_base, p.parts, parts_out, s)
-                        : launch_topk_prmt(a, k, metric, index_base, p.parts, parts_out, s);
+                        ? launch_topk_tc(a, k, metric, index_base, p.parts, parts_out, d.sms, s)
+                        : launch_topk_prmt(a, k, metric, index_base, p.parts, parts_out, d.sms, s);
     if (e != cudaSuccess) return cuda_status(e, "bolt_topk scan");
     if (p.parts > 1) return cuda_status(launch_merge(parts_out, p.parts, nq, k, out_keys, s), "bolt_topk merge");
     return BOLT_OK;
@@ -297,7 +308,7 @@ bolt_status bolt_topk(const uint32_t* codes, int64_t n, int m, const uint8_t* ql
 bolt_status bolt_topk_merge(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out_keys,
                             bolt_stream_t stream) {
     if (w < 1 || k < 1 || nq < 0) return fail(BOLT_E_SHAPE, "w, k must be >= 1, nq >= 0");
-    if ((int64_t)w * k > 8192) return fail(BOLT_E_SHAPE, "w*k = %lld > 8192", (long long)w * k);
+    if (w > kMaxParts || k > kMaxK) return fail(BOLT_E_SHAPE, "w = %d > 16384 or k = %d > 128", w, k);
     if (nq == 0) return BOLT_OK;
     if (!keys || !out_keys) return fail(BOLT_E_NULL, "bolt_topk_merge: NULL pointer");
     DevInfo d;

@@ -37,6 +37,27 @@ __device__ __forceinline__ uint64_t make_key(uint32_t kv, uint64_t gidx) {
     return (static_cast<uint64_t>(kv) << 48) | gidx;
 }
 
+// Number of row partitions for `tiles` query tiles over `groups` 8-row
+// groups and W resident warps (one warp task = one tile x one partition,
+// dealt round robin): at least 4 tasks per warp, at least
+// `min_groups_per_task` groups per task, and the partition count in a small
+// window that best fills the last round.
+inline int choose_parts(int64_t tiles, int64_t groups, int64_t W, int64_t min_groups_per_task) {
+    const int64_t max_parts = max64(1, min64(16384, groups / min_groups_per_task));
+    int64_t lo = max64(1, ceil_div(4 * W, tiles));
+    if (lo >= max_parts) return (int)max_parts;
+    const int64_t hi = min64(max_parts, 2 * lo + 8);
+    int64_t best = lo;
+    double best_eff = 0.0;
+    for (int64_t p = lo; p <= hi; ++p) {
+        const int64_t tasks = tiles * p;
+        const double eff = (double)tasks / (double)(ceil_div(tasks, W) * W);
+        if (eff > best_eff + 1e-9) { best_eff = eff; best = p; }
+        if (eff >= 0.97) break;
+    }
+    return (int)best;
+}
+
 // Per-launch argument block for the scan kernels.
 struct ScanArgs {
     const uint32_t* codes;
@@ -70,12 +91,13 @@ cudaError_t launch_scan_full(const ScanArgs& a, uint16_t* out16, float* out32, i
 // top-k (PRMT variant): partial lists [parts][nq][k] in ws, then merge
 int topk_prmt_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
 cudaError_t launch_topk_prmt(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
-                             uint64_t* part_keys, cudaStream_t s);
+                             uint64_t* part_keys, int sms, cudaStream_t s);
 // top-k (tcgen05 variant)
 int topk_tc_supported(int64_t n, int m, int64_t nq, int k);
 int topk_tc_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
 cudaError_t launch_topk_tc(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
-                           uint64_t* part_keys, cudaStream_t s);
+                           uint64_t* part_keys, int sms, cudaStream_t s);
+constexpr int kMaxParts = 16384;  // merge limit (shared memory of the tournament merge)
 
 cudaError_t launch_merge(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out,
                          cudaStream_t s);

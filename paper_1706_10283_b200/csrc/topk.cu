@@ -11,38 +11,53 @@ namespace {
 
 constexpr int kMergeThreads = 256;
 
-// One block per query: bitonic sort of the w*k candidates in shared memory.
+// One block per query: a k-round tournament over the heads of the w sorted
+// lists (head keys and read positions in shared memory).  Each round the
+// block finds the smallest head (ties impossible: keys are unique except
+// the UINT64_MAX padding), emits it and advances that list.
 __global__ void __launch_bounds__(kMergeThreads)
-merge_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int k, int pow2,
-             uint64_t* __restrict__ out) {
-    extern __shared__ uint64_t mbuf[];
+merge_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int k, uint64_t* __restrict__ out) {
+    extern __shared__ uint64_t mhead[];
+    int* mpos = reinterpret_cast<int*>(mhead + w);
+    __shared__ uint64_t wkey[kMergeThreads / 32];
+    __shared__ int wlist[kMergeThreads / 32];
     const int64_t q = blockIdx.x;
-    const int total = w * k;
-    for (int e = threadIdx.x; e < pow2; e += blockDim.x) {
-        uint64_t v = ~0ull;
-        if (e < total) {
-            const int s = e / k, p = e - s * k;
-            v = keys[((int64_t)s * nq + q) * k + p];
-        }
-        mbuf[e] = v;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    for (int p = threadIdx.x; p < w; p += blockDim.x) {
+        mhead[p] = keys[((int64_t)p * nq + q) * k];
+        mpos[p] = 0;
     }
     __syncthreads();
-    for (int size = 2; size <= pow2; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int e = threadIdx.x; e < pow2 / 2; e += blockDim.x) {
-                const int lo = 2 * e - (e & (stride - 1));
-                const int hi = lo + stride;
-                const bool asc = (lo & size) == 0;
-                const uint64_t a = mbuf[lo], b = mbuf[hi];
-                if ((a > b) == asc) {
-                    mbuf[lo] = b;
-                    mbuf[hi] = a;
-                }
-            }
-            __syncthreads();
+    for (int r = 0; r < k; ++r) {
+        uint64_t best = ~0ull;
+        int bi = -1;
+        for (int p = threadIdx.x; p < w; p += blockDim.x) {
+            const uint64_t h = mhead[p];
+            if (h < best) { best = h; bi = p; }
         }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const uint64_t ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (ob < best || (ob == best && (unsigned)oi < (unsigned)bi)) { best = ob; bi = oi; }
+        }
+        if (lane == 0) { wkey[warp] = best; wlist[warp] = bi; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int t = 1; t < nwarps; ++t)
+                if (wkey[t] < best || (wkey[t] == best && (unsigned)wlist[t] < (unsigned)bi)) {
+                    best = wkey[t];
+                    bi = wlist[t];
+                }
+            out[q * k + r] = best;
+            if (bi >= 0 && best != ~0ull) {
+                const int np = ++mpos[bi];
+                mhead[bi] = np < k ? keys[((int64_t)bi * nq + q) * k + np] : ~0ull;
+            }
+        }
+        __syncthreads();
     }
-    for (int p = threadIdx.x; p < k; p += blockDim.x) out[q * k + p] = mbuf[p];
 }
 
 __global__ void keys_split_kernel(const uint64_t* __restrict__ keys, int64_t count, int metric,
@@ -66,12 +81,10 @@ __global__ void keys_split_kernel(const uint64_t* __restrict__ keys, int64_t cou
 cudaError_t launch_merge(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out,
                          cudaStream_t s) {
     if (nq == 0) return cudaSuccess;
-    int pow2 = 1;
-    while (pow2 < w * k) pow2 <<= 1;
-    if (pow2 < 2) pow2 = 2;
-    size_t smem = (size_t)pow2 * sizeof(uint64_t);
+    const size_t smem = (size_t)w * (sizeof(uint64_t) + sizeof(int));
+    const int threads = w >= kMergeThreads ? kMergeThreads : (int)(((w + 31) / 32) * 32);
     cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    merge_kernel<<<(unsigned)nq, kMergeThreads, smem, s>>>(keys, w, nq, k, pow2, out);
+    merge_kernel<<<(unsigned)nq, threads, smem, s>>>(keys, w, nq, k, out);
     return cudaGetLastError();
 }
 

@@ -187,6 +187,33 @@ def test_topk_prmt_bitexact(bolt, orc, metric, n, m, nq, k, hi, base):
     np.testing.assert_array_equal(got, ref)
 
 
+TC_CASES = [
+    # n, m, nq, k, lut_hi, index_base -- tcgen05 variant: m in {8, 16, 32}, k <= 32
+    (1, 16, 1, 1, 256, 0),
+    (5, 8, 3, 10, 256, 0),
+    (300, 16, 129, 10, 4, 7),          # two query tiles, heavy ties, ragged tile
+    (4097, 16, 33, 10, 16, 0),
+    (2500, 8, 200, 32, 8, 123456),
+    (3000, 32, 7, 17, 256, 0),
+    (65537, 16, 130, 10, 8, 0),        # several row partitions + tail
+    (20000, 32, 64, 30, 256, 2**40),
+    (20000, 16, 64, 32, 256, 2**40),
+    (100000, 16, 300, 10, 256, 0),
+]
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+@pytest.mark.parametrize("n,m,nq,k,hi,base", TC_CASES)
+def test_topk_tc_bitexact(bolt, orc, metric, n, m, nq, k, hi, base):
+    """tcgen05 one-hot x table contraction: same integers, same keys."""
+    flat = G.random_codes(n, m, n + m + k + 1)
+    ql = G.random_qluts(nq, m, nq + k + 1, hi=hi)
+    ref = orc.topk(flat, ql, k, metric, index_base=base)
+    got = host(bolt.topk(pack_on_gpu(bolt, flat), n, dev(ql), k, metric, index_base=base,
+                         variant=bolt.VARIANT_TC))
+    np.testing.assert_array_equal(got, ref)
+
+
 def test_topk_constant_tables_all_ties(bolt, orc):
     """Every distance equal: the answer is the k lowest indices."""
     n, m, nq, k = 3001, 16, 4, 50
@@ -288,3 +315,52 @@ def test_c2_full_size_sampled(bolt, orc):
     qs = np.random.default_rng(2).choice(cfg.nq, 16, replace=False)
     qlh = host(ql)
     np.testing.assert_array_equal(keys[qs], orc.topk(gcodes, qlh[qs], cfg.k, 0))
+
+
+# ------------------------------------------------------- offline fit (f1)
+@pytest.mark.parametrize("cfg_name,n", [("c1", 10_000), ("c2", 20_000), ("c4", 5_000)])
+def test_kmeans_gpu_equals_oracle(bolt, orc, cfg_name, n):
+    """GPU k-means follows the oracle's fp64 operation order exactly (R8), so
+    the fp32 codebooks agree bit for bit."""
+    cfg = G.CONFIGS[cfg_name]
+    train = G.training(cfg, n)
+    init = G.kmeans_init_all(cfg, n)
+    ref = orc.fit(train, cfg.m, init, 6)
+    got = host(bolt.kmeans(dev(train), cfg.m, dev(init), 6))
+    np.testing.assert_array_equal(got, ref)
+
+
+def test_kmeans_gpu_empty_cluster(bolt, orc):
+    pts = np.array([[0.0], [0.1], [0.2], [50.0]] + [[100.0 + i] for i in range(14)], np.float32)
+    init = np.array([[0, 0] + list(range(4, 18))])
+    np.testing.assert_array_equal(host(bolt.kmeans(dev(pts), 1, dev(init), 3)), orc.fit(pts, 1, init, 3))
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+@pytest.mark.parametrize("cfg_name", ["c1", "c2", "c3"])
+def test_calibrate_gpu_equals_oracle(bolt, orc, cfg_name, metric):
+    cfg = G.CONFIGS[cfg_name]
+    train = G.training(cfg, 4000)
+    C = orc.fit(train, cfg.m, G.kmeans_init_all(cfg, len(train)), 3)
+    calib = G.calibration(cfg, train)[:300]
+    D = orc.luts(calib, C, metric)
+    a_ref, b_ref, alpha_ref, mse_ref = orc.calibrate(D)
+    a, b, am = bolt.calibrate(dev(D))
+    am = host(am)
+    np.testing.assert_array_equal(am[1:], mse_ref)
+    assert am[0] == alpha_ref
+    assert host(a)[0] == np.float32(a_ref)
+    np.testing.assert_array_equal(host(b), b_ref.astype(np.float32))
+
+
+def test_model_fit_on_gpu(bolt, orc):
+    cfg = G.CONFIGS["c1"]
+    X = G.database(cfg)
+    init = G.kmeans_init_all(cfg, len(X))
+    calib = G.calibration(cfg, X)
+    model = bolt.BoltModel.fit(dev(X), cfg.m, dev(init), dev(calib), 0, iters=cfg.kmeans_iters)
+    C = orc.fit(X, cfg.m, init, cfg.kmeans_iters)
+    np.testing.assert_array_equal(host(model.C), C)
+    a, b, alpha = orc.fit_quantizer(calib, C, 0)
+    assert model.a == float(a) and model.alpha == alpha
+    np.testing.assert_array_equal(host(model.b), b)
