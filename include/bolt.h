@@ -206,6 +206,13 @@ BOLT_API size_t bolt_calibrate_workspace_bytes(int64_t nq, int m);
 BOLT_API bolt_status bolt_calibrate(const double* luts, int64_t nq, int m, float* a_out, float* b_out,
                            double* alpha_mse_out, void* ws, size_t ws_bytes, bolt_stream_t stream);
 
+/* ------------------------------------------------------------ diagnostics */
+/* (host) Copy up to n internal kernel cycle counters to host `out` and reset
+ * them.  All zeros unless the library was built with -DBOLT_PROFILE
+ * (python -m paper_1706_10283_b200.build --profile); used by tools/ only.
+ * Returns the number of counters written. */
+BOLT_API int bolt_debug_counters(uint64_t* out, int n);
+
 #ifdef __cplusplus
 }
 #endif

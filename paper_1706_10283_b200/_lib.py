@@ -44,6 +44,7 @@ SIGNATURES = {
     "bolt_kmeans": ([_P, _I64, _I32, _I64, _I32, _P, _I32, _P, _P, _SZ, _P], _I32),
     "bolt_calibrate_workspace_bytes": ([_I64, _I32], _SZ),
     "bolt_calibrate": ([_P, _I64, _I32, _P, _P, _P, _P, _SZ, _P], _I32),
+    "bolt_debug_counters": ([_P, _I32], _I32),
 }
 
 

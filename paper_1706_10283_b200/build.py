@@ -56,7 +56,12 @@ def _compile(src, verbose):
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+    """profile=True adds -DBOLT_PROFILE (cycle counters, tools/ only)."""
+    global NVCC_FLAGS
+    if profile:
+        NVCC_FLAGS = NVCC_FLAGS + ["-DBOLT_PROFILE"]
+        force = True
     os.makedirs(OBJ, exist_ok=True)
     if not force and not _stale(LIB, _deps()):
         return LIB
@@ -80,4 +85,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    print(build(force="--force" in sys.argv or "--profile" in sys.argv, verbose="--verbose" in sys.argv,
+                profile="--profile" in sys.argv))

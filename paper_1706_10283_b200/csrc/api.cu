@@ -97,12 +97,19 @@ TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     p.variant = v;
     p.parts = v == BOLT_VARIANT_TC ? topk_tc_parts(n, m, nq, k, sms) : topk_prmt_parts(n, m, nq, k, sms);
     p.ws = p.parts > 1 ? (size_t)p.parts * nq * k * sizeof(uint64_t) : 0;
+    // both variants keep a per-query shared threshold array (u32) after the partial lists
+    if (p.ws > 0) p.ws += (size_t)nq * sizeof(uint32_t);
     return p;
 }
 
 }  // namespace
 
 extern "C" {
+
+int bolt_debug_counters(uint64_t* out, int n) {
+    if (!out || n <= 0) return 0;
+    return tc_debug_counters(out, n < kNumCounters ? n : kNumCounters);
+}
 
 const char* bolt_version(void) { return "bolt-b200 1.0 (abi 1, sm_100a)"; }
 

@@ -58,6 +58,17 @@ inline int choose_parts(int64_t tiles, int64_t groups, int64_t W, int64_t min_gr
     return (int)best;
 }
 
+// Diagnostic cycle counters (BOLT_PROFILE builds only).
+constexpr int kNumCounters = 16;
+#ifdef BOLT_PROFILE
+// defined (per translation unit that uses it) by BOLT_DEFINE_COUNTERS
+#define BOLT_PROF_ADD(i, v) atomicAdd(&g_counters[(i)], (unsigned long long)(v))
+#define BOLT_CLOCK() clock64()
+#else
+#define BOLT_PROF_ADD(i, v) ((void)0)
+#define BOLT_CLOCK() 0ll
+#endif
+
 // Per-launch argument block for the scan kernels.
 struct ScanArgs {
     const uint32_t* codes;
@@ -99,6 +110,7 @@ cudaError_t launch_topk_tc(const ScanArgs& a, int k, int metric, int64_t index_b
                            uint64_t* part_keys, int sms, cudaStream_t s);
 constexpr int kMaxParts = 16384;  // merge limit (shared memory of the tournament merge)
 
+int tc_debug_counters(uint64_t* out, int n);  // scan_tc.cu (BOLT_PROFILE builds)
 cudaError_t launch_merge(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out,
                          cudaStream_t s);
 cudaError_t launch_keys_split(const uint64_t* keys, int64_t count, int metric, uint16_t* vals,

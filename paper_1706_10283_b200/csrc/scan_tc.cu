@@ -10,17 +10,22 @@
 // integer as the PRMT scan, bit for bit.  It executes 16x the algorithmic
 // lookups, at tensor-core rate.
 //
-// Per CTA (one per SM): a tile of 128 queries (MMA M) against a contiguous
-// range of database vectors in tiles of N vectors (N = 256 for M <= 16).
-//   warps 0-3  producers: stage A once (16-byte units, K-major "interleave"
-//              layout), then expand each vector tile's codes into the one-hot
-//              B tile in shared memory (one aligned 16-byte store per
-//              (vector, codebook)), double-buffered.
-//   warp  8    MMA issuer (one thread): M/2 x tcgen05.mma (K = 32 bytes each)
-//              into one of two TMEM accumulators, commit to mbarriers.
-//   warps 4-7  epilogue: thread = query (TMEM lane); tcgen05.ld the N sums,
-//              min/max-reduce against the query's running top-k threshold,
-//              rare inserts into the query's sorted key list (shared memory).
+// A CTA pair (cluster of 2, cta_group::2) computes 256 queries x 256
+// vectors per MMA tile: CTA r holds queries [128r, 128r+128) of the query
+// tile (its half of A) and vectors [128r, 128r+128) of each vector tile (its
+// half of B); its TMEM receives its 128 queries x all 256 vectors.  So each
+// SM expands only 128 one-hot vectors per 1024-cycle MMA tile.
+//   warps 0-3   producers: stage A once (16-byte units, K-major "interleave"
+//               layout), then expand each vector tile's codes into the one-hot
+//               B half in shared memory (one aligned 16-byte store per
+//               (vector, codebook)), STAGES-deep ring.
+//   warps 4-11  epilogue: thread = query (TMEM lane), two warps per lane
+//               quadrant splitting the 256 columns; tcgen05.ld .pack::16b the
+//               sums, packed u16x2 min/max tree against the query's running
+//               top-k threshold, rare inserts into a register top-k list.
+//   warp  12    MMA issuer (leader CTA, one thread): M/2 tcgen05.mma
+//               (K = 32 bytes each) into one of two TMEM accumulators; commits
+//               multicast to both CTAs' mbarriers.
 // Shared-memory operand layout (both K-major, SWIZZLE_NONE): the 16-byte
 // chunk j of row r lives at j * (rows * 16) + (r / 8) * 128 + (r % 8) * 16,
 // so SBO (next 8 rows) = 128 B and LBO (next 16-byte K chunk) = rows * 16 B.
@@ -28,31 +33,60 @@
 #include "topk_list.cuh"
 
 namespace bolt {
+#ifdef BOLT_PROFILE
+__device__ unsigned long long g_counters[kNumCounters];
+#endif
+
+int tc_debug_counters(uint64_t* out, int n) {
+#ifdef BOLT_PROFILE
+    unsigned long long h[kNumCounters] = {};
+    cudaMemcpyFromSymbol(h, g_counters, sizeof(h));
+    unsigned long long z[kNumCounters] = {};
+    cudaMemcpyToSymbol(g_counters, z, sizeof(z));
+    for (int i = 0; i < n; ++i) out[i] = h[i];
+#else
+    for (int i = 0; i < n; ++i) out[i] = 0;
+#endif
+    return n;
+}
+
 namespace tc {
 
-constexpr int kQM = 128;                 // queries per tile = MMA M = TMEM lanes
+constexpr int kQM = 128;                 // queries per CTA = TMEM lanes (MMA M = 256 per pair)
 constexpr int kProducers = 128;
 constexpr int kEpiWarps = 8;             // two warps per TMEM lane quadrant (column halves)
 constexpr int kEpilogue = kEpiWarps * 32;
 constexpr int kMmaWarp = 4 + kEpiWarps;
 constexpr int kThreads = (kMmaWarp + 1) * 32;  // 4 producer + 8 epilogue + 1 MMA warp
 constexpr int kMaxTopk = 32;
+constexpr int kScratchStride = 20;       // u32 words per epilogue thread: 32 u16 values + pad
 
 template <int M>
 struct Cfg {
-    static constexpr int K = 16 * M;                        // bytes per row
-    static constexpr int N = (4096 / M) < 256 ? (4096 / M) : 256;  // vectors per tile
+    static constexpr int K = 16 * M;                      // bytes per row
+    static constexpr int N = 256;                         // vectors per MMA tile (pair)
+    static constexpr int NH = N / 2;                      // vectors per CTA (its half of B)
     static constexpr int A_BYTES = kQM * K;
-    static constexpr int B_BYTES = N * K;
+    static constexpr int B_BYTES = NH * K;                // one stage of this CTA's half of B
+    static constexpr int SCRATCH_BYTES = kEpilogue * kScratchStride * 4;
+    static constexpr int STAGES_RAW = (220 * 1024 - A_BYTES - SCRATCH_BYTES) / (B_BYTES + NH * M / 2);
+    static constexpr int STAGES = STAGES_RAW > 4 ? 4 : STAGES_RAW;
+    static_assert(STAGES >= 2, "shared memory too small for a double-buffered B tile");
     static constexpr int KSTEPS = K / 32;
-    static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : (2 * N <= 64 ? 64 : (2 * N <= 128 ? 128 : (2 * N <= 256 ? 256 : 512)));
-    // dynamic smem: A | B0 | B1 | code stages [2][N*M/8] u32 | barriers
-    static constexpr int STAGE_OFF = A_BYTES + 2 * B_BYTES;
-    static constexpr int BAR_OFF = STAGE_OFF + 2 * N * M / 2;
-    static constexpr int SMEM = BAR_OFF + 128;
+    static constexpr int TMEM_COLS = 512;                  // 2 x 256-column accumulators
+    // 32-bit epilogue keys: kv' <= 255 M needs VAL_BITS, the rest (to 31 bits) index the pair's range
+    static constexpr int VAL_BITS = M <= 8 ? 11 : (M <= 16 ? 12 : 13);
+    static constexpr int IDX_BITS = 31 - VAL_BITS;
+    static constexpr int64_t MAX_RANGE = int64_t(1) << IDX_BITS;
+    static constexpr uint32_t KVMAX = 255u * M;
+    // dynamic smem: A | B[STAGES] | code stages [STAGES][NH*M/8] u32 | scratch | barriers
+    static constexpr int CODE_OFF = A_BYTES + STAGES * B_BYTES;
+    static constexpr int SCRATCH_OFF = CODE_OFF + STAGES * NH * M / 2;
+    static constexpr int BAR_OFF = SCRATCH_OFF + SCRATCH_BYTES;
+    static constexpr int SMEM = BAR_OFF + 256;
     // instruction descriptor: D s32 (bits 4-5 = 2), A/B u8 (format 0), K-major,
-    // N >> 3 at bit 17, M >> 4 at bit 24
-    static constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kQM >> 4) << 24);
+    // N >> 3 at bit 17, M >> 4 at bit 24 (M = 256 for the pair)
+    static constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -76,6 +110,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the mbarrier at the same shared-memory offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 remote;\n\t"
+        "mapa.shared::cluster.u32 remote, %0, %1;\n\t"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [remote];\n\t}" ::"r"(smem_u32(bar)),
+        "r"(cta)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n"
+        "DONE:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -88,17 +150,21 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
            ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
 }
 
-__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void mma_i8_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
 }
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
+// commit the leader's MMAs to the barrier at the same offset in both CTAs
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -109,6 +175,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
           "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+// 32 columns as 16 registers: reg i = low16(col 2i) | low16(col 2i+1) << 16
+// (measured: tools/probe_tmem_pack.cu); exact since every sum is < 2^16.
+__device__ __forceinline__ void tmem_ld16p(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+        "%12, %13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -131,28 +207,30 @@ __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
     return r;
 }
 
-// Register-resident sorted top-k list of one thread, right-aligned in KMAX
-// slots: slots [0, KMAX-k) hold 0 (passes every key through), slots
-// [KMAX-k, KMAX) the k best keys ascending, so the k-th best is always
-// slot KMAX-1.  Insert = one branch-free bubble pass.
+// Register-resident sorted top-k list of one thread with 32-bit keys
+// (kv' << IDX_BITS) | local index (kv' = acc for L2, 255 M - acc for dot, so
+// smaller is better in both cases; local = vector index within the CTA's
+// range), right-aligned in KMAX slots: slots [0, KMAX-k) hold 0 (every key
+// passes through them), slots [KMAX-k, KMAX) the k best keys ascending, so
+// the k-th best is always slot KMAX-1.  Keys are unique, so an insert is a
+// branch-free bubble pass of min/max pairs.
 template <int KMAX>
 struct RegList {
-    uint64_t v[KMAX];
+    uint32_t v[KMAX];
     __device__ __forceinline__ void init(int k) {
 #pragma unroll
-        for (int i = 0; i < KMAX; ++i) v[i] = i < KMAX - k ? 0ull : ~0ull;
+        for (int i = 0; i < KMAX; ++i) v[i] = i < KMAX - k ? 0u : 0xFFFFFFFFu;
     }
-    __device__ __forceinline__ void insert(uint64_t c) {
+    __device__ __forceinline__ void insert(uint32_t c) {
 #pragma unroll
         for (int i = 0; i < KMAX; ++i) {
-            const bool lt = v[i] < c;
-            const uint64_t lo = lt ? v[i] : c;
-            c = lt ? c : v[i];
+            const uint32_t lo = min(v[i], c);
+            c = max(v[i], c);
             v[i] = lo;
         }
     }
-    __device__ __forceinline__ uint32_t threshold() const {
-        return v[KMAX - 1] == ~0ull ? kNotFull : (uint32_t)(v[KMAX - 1] >> 48);
+    __device__ __forceinline__ uint32_t threshold(int idx_bits) const {
+        return v[KMAX - 1] == 0xFFFFFFFFu ? kNotFull : (v[KMAX - 1] >> idx_bits);
     }
 };
 
@@ -162,225 +240,335 @@ struct RegList {
 namespace bolt {
 namespace tc {
 
+// Candidate mask of 32 packed u16 sums p[16] (value j = half j&1 of p[j>>1])
+// against the threshold: SWAR compare of both halves (values and threshold
+// < 2^15), flags gathered with PRMT.  Bit 8k + i of the result <-> value
+// 4i + k.
+template <bool kDot>
+__device__ __forceinline__ uint32_t candidate_mask(const uint32_t (&p)[16], uint32_t tp) {
+    uint32_t nm = 0;  // 1 = not a candidate
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t d0 = kDot ? ((tp | 0x80008000u) - p[2 * i]) : ((p[2 * i] | 0x80008000u) - tp);
+        const uint32_t d1 = kDot ? ((tp | 0x80008000u) - p[2 * i + 1]) : ((p[2 * i + 1] | 0x80008000u) - tp);
+        const uint32_t x = __byte_perm(d0, d1, 0x7531);  // flags at bits 7, 15, 23, 31
+        nm |= (x >> (7 - i)) & (0x01010101u << i);
+    }
+    return ~nm;
+}
+
 template <int M, bool kDot, int KMAX>
 __global__ void __launch_bounds__(kThreads, 1)
-topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int parts, int64_t vpp, int tiles_q,
-               uint64_t* __restrict__ part_keys) {
+topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, uint64_t* __restrict__ part_keys,
+               uint32_t* __restrict__ gthr_inv) {
     using C = Cfg<M>;
+    constexpr int S = C::STAGES;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sA = smem;
     uint8_t* sB = smem + C::A_BYTES;
-    uint32_t* stages = reinterpret_cast<uint32_t*>(smem + C::STAGE_OFF);
+    uint32_t* codes_st = reinterpret_cast<uint32_t*>(smem + C::CODE_OFF);
+    uint32_t* scratch_all = reinterpret_cast<uint32_t*>(smem + C::SCRATCH_OFF);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
-    uint64_t* full = bars;            // [2] producers -> MMA (count 128)
-    uint64_t* empty = bars + 2;       // [2] MMA commit -> producers
-    uint64_t* tfull = bars + 4;       // [2] MMA commit -> epilogue
-    uint64_t* tempty = bars + 6;      // [2] epilogue -> MMA (count 128)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    uint64_t* full = bars;                 // [S]  leader: producers of both CTAs -> MMA
+    uint64_t* empty = bars + S;            // [S]  both: MMA commit -> producers
+    uint64_t* tfull = bars + 2 * S;        // [2]  both: MMA commit -> epilogue
+    uint64_t* tempty = bars + 2 * S + 2;   // [2]  leader: epilogues of both CTAs -> MMA
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int unit = blockIdx.x;
+    const uint32_t rank = cluster_rank();
+    const int unit = blockIdx.x >> 1;
     const int tq = unit % tiles_q;
     const int part = unit / tiles_q;
-    const int64_t q0 = (int64_t)tq * kQM;
+    const int64_t q0 = (int64_t)tq * 2 * kQM + rank * kQM;  // this CTA's queries
     const int64_t vbeg = (int64_t)part * vpp;
     const int64_t vend = min64(a.n, vbeg + vpp);
     const int ntiles = vend > vbeg ? (int)ceil_div(vend - vbeg, C::N) : 0;
 
     if (threadIdx.x == 0) {
-        mbar_init(&full[0], kProducers);
-        mbar_init(&full[1], kProducers);
-        mbar_init(&empty[0], 1);
-        mbar_init(&empty[1], 1);
-        mbar_init(&tfull[0], 1);
-        mbar_init(&tfull[1], 1);
-        mbar_init(&tempty[0], kEpilogue);
-        mbar_init(&tempty[1], kEpilogue);
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 2);    // one arrive per CTA (after a producer named barrier)
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 2 * kEpiWarps);  // one arrive per epilogue warp of both CTAs
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kMmaWarp) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"((uint32_t)C::TMEM_COLS)
                      : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
     }
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const long long tk0 = BOLT_CLOCK();
 
     if (warp < 4) {
         // ------------------------------------------------------ producers
         const int t = threadIdx.x;
-        // A: query tables, 16-byte unit (c, q) -> c * (128*16) + (q/8)*128 + (q%8)*16
+        // A: this CTA's 128 queries, 16-byte unit (c, q) -> c*(128*16) + (q/8)*128 + (q%8)*16
         for (int u = t; u < kQM * M; u += kProducers) {
             const int c = u / kQM, q = u % kQM;
             uint4 v = make_uint4(0, 0, 0, 0);
             if (q0 + q < a.nq) v = __ldg(reinterpret_cast<const uint4*>(a.qluts + ((q0 + q) * M + c) * kK));
             *reinterpret_cast<uint4*>(sA + c * (kQM * 16) + (q >> 3) * 128 + (q & 7) * 16) = v;
         }
-        // codes of a tile = N/8 groups x M words, contiguous: one uint4 per thread
-        constexpr int kChunks = C::N * M / 32;  // uint4 per tile (<= 128)
-        static_assert(kChunks <= kProducers, "tile code block must fit one uint4 per producer");
+        // codes of this CTA's half tile = NH/8 groups x M words, contiguous
+        constexpr int kChunks = C::NH * M / 32;  // uint4 per half tile (<= 128)
+        static_assert(kChunks <= kProducers, "half-tile code block must fit one uint4 per producer");
         const int64_t words_total = a.groups * M;
         auto load_chunk = [&](int tile) -> uint4 {
-            const int64_t w0 = ((vbeg + (int64_t)tile * C::N) >> 3) * M + (int64_t)t * 4;
+            const int64_t w0 = ((vbeg + (int64_t)tile * C::N + rank * C::NH) >> 3) * M + (int64_t)t * 4;
             if (t < kChunks && w0 < words_total) return __ldg(reinterpret_cast<const uint4*>(a.codes + w0));
             return make_uint4(0, 0, 0, 0);
         };
         uint4 pre = ntiles > 0 ? load_chunk(0) : make_uint4(0, 0, 0, 0);
-        constexpr int kVecPerThread = C::N / kProducers > 0 ? C::N / kProducers : 1;
         for (int tile = 0; tile < ntiles; ++tile) {
-            const int s = tile & 1;
-            mbar_wait(&empty[s], ((tile >> 1) & 1) ^ 1);
-            uint32_t* stage = stages + s * (C::N * M / 8);
-            if (t < kChunks) reinterpret_cast<uint4*>(stage)[t] = pre;
+            const int s = tile % S;
+            long long tw0 = BOLT_CLOCK();
+            mbar_wait(&empty[s], ((tile / S) & 1) ^ 1);
+            if (t == 0) BOLT_PROF_ADD(0, BOLT_CLOCK() - tw0);  // producer waits on empty
+            uint32_t* cst = codes_st + s * (C::NH * M / 8);
+            if (t < kChunks) reinterpret_cast<uint4*>(cst)[t] = pre;
             asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");
             if (tile + 1 < ntiles) pre = load_chunk(tile + 1);
             uint8_t* b = sB + s * C::B_BYTES;
-            const int64_t tb = vbeg + (int64_t)tile * C::N;
-#pragma unroll
-            for (int h = 0; h < kVecPerThread; ++h) {
-                const int v = t + h * kProducers;
-                if (v >= C::N) break;
-                const bool valid = tb + v < vend;
-                const uint32_t* wv = stage + (v >> 3) * M;
-                const uint32_t sh = (v & 7) * 4;
+            const int64_t hb = vbeg + (int64_t)tile * C::N + rank * C::NH;  // first vector of this half
+            const int v = t;                                               // NH == kProducers
+            const uint32_t* wv = cst + (v >> 3) * M;
+            const uint32_t sh = (v & 7) * 4;
+            if (hb + C::NH <= vend) {
 #pragma unroll
                 for (int c4 = 0; c4 < M; c4 += 4) {
                     const uint4 w = *reinterpret_cast<const uint4*>(wv + c4);
                     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint32_t sbits = valid ? ((ws[j] >> sh) & 0xFu) * 8u : 128u;  // 128 -> zeros
-                        *reinterpret_cast<uint4*>(b + (c4 + j) * (C::N * 16) + v * 16) = one_hot16_s(sbits);
-                    }
+                    for (int j = 0; j < 4; ++j)
+                        *reinterpret_cast<uint4*>(b + (c4 + j) * (C::NH * 16) + v * 16) =
+                            one_hot16_s(((ws[j] >> sh) & 0xFu) * 8u);
                 }
+            } else {  // last, partial tile: rows past the range are all-zero
+                const bool valid = hb + v < vend;
+#pragma unroll 1
+                for (int c = 0; c < M; ++c)
+                    *reinterpret_cast<uint4*>(b + c * (C::NH * 16) + v * 16) =
+                        one_hot16_s(valid ? ((wv[c] >> sh) & 0xFu) * 8u : 128u);
             }
             fence_proxy_async();
-            mbar_arrive(&full[s]);
+            asm volatile("bar.sync 2, %0;" ::"n"(kProducers) : "memory");
+            if (t == 0) {
+                if (rank == 0) mbar_arrive(&full[s]);
+                else mbar_arrive_cluster(&full[s], 0);
+            }
         }
     } else if (warp < 4 + kEpiWarps) {
         // ------------------------------------------------------- epilogue
         const int quad = warp & 3;                 // TMEM lanes 32*quad .. (warp % 4 rule)
         const int half = (warp - 4) >> 2;          // column half of the tile
-        const int q = quad * 32 + lane;            // query row of the tile
+        const int q = quad * 32 + lane;            // query row of this CTA
         constexpr int kCols = C::N / 2;
+        uint32_t* scratch = scratch_all + (threadIdx.x - 128) * kScratchStride;
         RegList<KMAX> list;
         list.init(k);
+        // Thresholds in kv' units.  own = k-th key of this list; shared =
+        // min over every list of this query (all CTAs), kept in global memory
+        // as 0xFFFF - T so that a zeroed word means "none" (T = 0xFFFF).  A
+        // value can reach the global top-k only if kv' < own and kv' <= T.
+        uint32_t own = kNotFull;
+        uint32_t published = kNotFull;
+        const bool qvalid = q0 + q < a.nq;
+        uint32_t* gq = gthr_inv + (qvalid ? q0 + q : 0);
         uint32_t thr = kNotFull;
+        uint32_t g_next = 0;  // inverted shared threshold (0 = none yet)
         const uint32_t tlane = (uint32_t)(quad * 32) << 16;
         for (int tile = 0; tile < ntiles; ++tile) {
             const int d = tile & 1;
+            long long tw0 = BOLT_CLOCK();
             mbar_wait(&tfull[d], (tile >> 1) & 1);
+            if (threadIdx.x == 128) BOLT_PROF_ADD(1, BOLT_CLOCK() - tw0);  // epilogue waits on tfull
             tc_fence_after();
-            const int64_t tb = vbeg + (int64_t)tile * C::N;
-            const int nvalid = (int)min64(C::N, vend - tb);
-#pragma unroll 1
-            for (int col = half * kCols; col < (half + 1) * kCols; col += 32) {
-                const uint32_t tcol = tmem + tlane + (uint32_t)(d * C::N + col);
-                uint32_t r[32];
-                tmem_ld32(tcol, r);
-                tmem_wait_ld();
-                // tree reduction on a copy: best (smallest kv) of the 32 columns
-                uint32_t t[16];
+            // copy this warp's 128 columns out of TMEM (packed u16 pairs) and
+            // release the accumulator at once, so that a slow filter pass on
+            // this warp never holds the MMA back
+            uint32_t p[4][16];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) t[j] = kDot ? max(r[j], r[j + 16]) : min(r[j], r[j + 16]);
+            for (int c = 0; c < 4; ++c)
+                tmem_ld16p(tmem + tlane + (uint32_t)(d * C::N + half * kCols + c * 32), p[c]);
+            tmem_wait_ld();
+            if (threadIdx.x == 128) BOLT_PROF_ADD(2, BOLT_CLOCK() - tw0);  // wait + TMEM load
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (rank == 0) mbar_arrive(&tempty[d]);
+                else mbar_arrive_cluster(&tempty[d], 0);
+            }
+            const long long tp0 = BOLT_CLOCK();
+            // shared threshold: use the value fetched one tile ago, prefetch the next
+            thr = min(own, 0xFFFFu - g_next + 1u);
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g_next) : "l"(gq));
+            const int tbl = tile * C::N;  // local index of the tile's first vector
+            const int nvalid = (int)min64(C::N, vend - vbeg - tbl);
+            // packed u16x2 tree over the warp's 128 columns; the four chunk
+            // (32-column) minima route the slow path
+            uint32_t cb[4];
 #pragma unroll
-                for (int w = 8; w > 0; w >>= 1)
+            for (int c = 0; c < 4; ++c) {
+                uint32_t g[6];
 #pragma unroll
-                    for (int j = 0; j < w; ++j) t[j] = kDot ? max(t[j], t[j + w]) : min(t[j], t[j + w]);
-                const uint32_t kvbest = kDot ? 0xFFFFu - t[0] : t[0];
-                const bool trig = kvbest < thr || col + 32 > nvalid;
-                if (!__any_sync(0xffffffffu, trig)) continue;
-                // slow path: per-lane candidate columns, then a warp-uniform walk
-                // over the union re-reading single TMEM columns
-                uint32_t mask = 0;
-                if (trig) {
+                for (int i = 0; i < 5; ++i)
+                    g[i] = kDot ? __vimax3_u16x2(p[c][3 * i], p[c][3 * i + 1], p[c][3 * i + 2])
+                                : __vimin3_u16x2(p[c][3 * i], p[c][3 * i + 1], p[c][3 * i + 2]);
+                g[5] = p[c][15];
+                cb[c] = kDot ? __vmaxu2(__vimax3_u16x2(g[0], g[1], g[2]), __vimax3_u16x2(g[3], g[4], g[5]))
+                             : __vminu2(__vimin3_u16x2(g[0], g[1], g[2]), __vimin3_u16x2(g[3], g[4], g[5]));
+            }
+            const uint32_t u = kDot ? __vimax3_u16x2(cb[0], cb[1], __vmaxu2(cb[2], cb[3]))
+                                    : __vimin3_u16x2(cb[0], cb[1], __vminu2(cb[2], cb[3]));
+            const uint32_t best = kDot ? max(u & 0xFFFFu, u >> 16) : min(u & 0xFFFFu, u >> 16);
+            const uint32_t kvbest = kDot ? C::KVMAX - best : best;
+            const bool tail = nvalid < C::N;
+            if (kvbest < thr || tail) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const uint32_t kv = kDot ? 0xFFFFu - r[j] : r[j];
-                        mask |= (kv < thr && col + j < nvalid) ? (1u << j) : 0u;
-                    }
-                }
-                uint32_t wm = __reduce_or_sync(0xffffffffu, mask);
-                while (wm) {
-                    const int j = __ffs(wm) - 1;
-                    wm &= wm - 1;
-                    const uint32_t v = tmem_ld1(tcol + j);
-                    tmem_wait_ld();
-                    const uint32_t kv = kDot ? 0xFFFFu - v : v;
-                    if (((mask >> j) & 1u) && kv < thr) {
-                        list.insert(make_key(kv, (uint64_t)(index_base + tb + col + j)));
-                        thr = list.threshold();
+                for (int c = 0; c < 4; ++c) {
+                    const int col = half * kCols + c * 32;
+                    const uint32_t cbest = kDot ? max(cb[c] & 0xFFFFu, cb[c] >> 16) : min(cb[c] & 0xFFFFu, cb[c] >> 16);
+                    const int nleft = nvalid - col;
+                    if ((kDot ? C::KVMAX - cbest : cbest) >= thr && nleft >= 32) continue;
+                    BOLT_PROF_ADD(9, 1);  // lane slow-path entries
+                    // slow path (lane-divergent): candidate mask, values parked in
+                    // this thread's scratch row, per-lane loop over its candidates
+                    uint32_t mask = thr == kNotFull ? 0xFFFFFFFFu
+                                                    : candidate_mask<kDot>(p[c], (kDot ? C::KVMAX - thr : thr) * 0x10001u);
+                    uint4* sv = reinterpret_cast<uint4*>(scratch);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        sv[i] = make_uint4(p[c][4 * i], p[c][4 * i + 1], p[c][4 * i + 2], p[c][4 * i + 3]);
+                    while (mask) {
+                        const int bpos = __ffs(mask) - 1;
+                        mask &= mask - 1;
+                        const int j = 4 * (bpos & 7) + (bpos >> 3);
+                        const uint32_t v = (scratch[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
+                        const uint32_t kv = kDot ? C::KVMAX - v : v;
+                        if (kv < thr && j < nleft) {
+                            list.insert((kv << C::IDX_BITS) | (uint32_t)(tbl + col + j));
+                            own = list.threshold(C::IDX_BITS);
+                            thr = min(thr, own);
+                            BOLT_PROF_ADD(10, 1);  // inserts
+                        }
                     }
                 }
             }
-            tc_fence_before();
-            mbar_arrive(&tempty[d]);
+            __syncwarp();  // reconverge before the next tile's .aligned tcgen05.ld
+            if (lane == 0) BOLT_PROF_ADD(8, BOLT_CLOCK() - tp0);  // processing cycles (all warps)
+            if (own < published && qvalid) {
+                published = own;
+                asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gq), "r"(0xFFFFu - own) : "memory");
+            }
         }
         if (q0 + q < a.nq) {
             uint64_t* dst = part_keys + ((int64_t)(2 * part + half) * a.nq + q0 + q) * k;
 #pragma unroll
-            for (int i = 0; i < KMAX; ++i)
-                if (i >= KMAX - k) dst[i - (KMAX - k)] = list.v[i];
+            for (int i = 0; i < KMAX; ++i) {
+                if (i >= KMAX - k) {
+                    const uint32_t key = list.v[i];
+                    uint64_t out = ~0ull;
+                    if (key != 0xFFFFFFFFu) {
+                        const uint32_t kvp = key >> C::IDX_BITS;
+                        const uint32_t kv64 = kDot ? 0xFFFFu - (C::KVMAX - kvp) : kvp;  // (R13) 0xFFFF - acc
+                        out = make_key(kv64, (uint64_t)(index_base + vbeg + (key & ((1u << C::IDX_BITS) - 1u))));
+                    }
+                    dst[i - (KMAX - k)] = out;
+                }
+            }
         }
-    } else if (warp == kMmaWarp) {
-        // ------------------------------------------------------ MMA issuer
+    } else if (warp == kMmaWarp && rank == 0) {
+        // ------------------------------------------- MMA issuer (leader CTA)
         if (lane == 0) {
             const uint32_t a_base = smem_u32(sA);
             const uint32_t b_base = smem_u32(sB);
             for (int tile = 0; tile < ntiles; ++tile) {
-                const int s = tile & 1, d = tile & 1;
-                mbar_wait(&full[s], (tile >> 1) & 1);
-                mbar_wait(&tempty[d], ((tile >> 1) & 1) ^ 1);
+                const int s = tile % S, d = tile & 1;
+                long long t0 = BOLT_CLOCK();
+                mbar_wait_cluster(&full[s], (tile / S) & 1);
+                long long t1 = BOLT_CLOCK();
+                mbar_wait_cluster(&tempty[d], ((tile >> 1) & 1) ^ 1);
+                long long t2 = BOLT_CLOCK();
+                BOLT_PROF_ADD(3, t1 - t0);  // MMA waits on full
+                BOLT_PROF_ADD(4, t2 - t1);  // MMA waits on tempty
+                BOLT_PROF_ADD(5, 1);        // tiles
                 tc_fence_after();
                 const uint32_t bs = b_base + s * C::B_BYTES;
 #pragma unroll
                 for (int ks = 0; ks < C::KSTEPS; ++ks) {
-                    // K step ks covers 16-byte chunks 2ks, 2ks+1
+                    // K step ks covers 16-byte chunks 2ks, 2ks+1 (same offsets in the peer CTA)
                     const uint64_t ad = smem_desc(a_base + 2 * ks * (kQM * 16), kQM * 16, 128);
-                    const uint64_t bd = smem_desc(bs + 2 * ks * (C::N * 16), C::N * 16, 128);
-                    mma_i8(tmem + (uint32_t)(d * C::N), ad, bd, C::IDESC, ks > 0 ? 1u : 0u);
+                    const uint64_t bd = smem_desc(bs + 2 * ks * (C::NH * 16), C::NH * 16, 128);
+                    mma_i8_pair(tmem + (uint32_t)(d * C::N), ad, bd, C::IDESC, ks > 0 ? 1u : 0u);
                 }
-                mma_commit(&empty[s]);
-                mma_commit(&tfull[d]);
+                mma_commit_pair(&empty[s]);
+                mma_commit_pair(&tfull[d]);
             }
         }
         __syncwarp();
     }
+    if (threadIdx.x == 0) BOLT_PROF_ADD(6, BOLT_CLOCK() - tk0);   // CTA main-loop cycles
+    if (threadIdx.x == 0) BOLT_PROF_ADD(7, 1);                    // CTAs
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();  // all MMAs done and consumed in both CTAs
     if (warp == kMmaWarp) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS)
                      : "memory");
     }
 }
 
 template <int M, bool kDot, int KMAX>
 cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, uint64_t* part_keys,
-                      cudaStream_t s) {
+                      uint32_t* gthr, cudaStream_t s) {
     using C = Cfg<M>;
-    const int tiles_q = (int)ceil_div(a.nq, kQM);
+    const int tiles_q = (int)ceil_div(a.nq, 2 * kQM);
     const int64_t vpp = ceil_div(ceil_div(a.n, rparts), 8) * 8;
-    const unsigned grid = (unsigned)(tiles_q * rparts);
-    cudaFuncSetAttribute(topk_tc_kernel<M, kDot, KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    topk_tc_kernel<M, kDot, KMAX><<<grid, kThreads, C::SMEM, s>>>(a, k, index_base, rparts, vpp, tiles_q,
-                                                                 part_keys);
-    return cudaGetLastError();
+    auto kern = topk_tc_kernel<M, kDot, KMAX>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * tiles_q * rparts));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)a.nq * sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+    return cudaLaunchKernelEx(&cfg, kern, a, k, index_base, vpp, tiles_q, part_keys, gthr);
 }
 
 template <int M>
 cudaError_t launch_m(const ScanArgs& a, int k, int metric, int64_t index_base, int rparts, uint64_t* part_keys,
-                     cudaStream_t s) {
+                     uint32_t* gthr, cudaStream_t s) {
     const bool dot = metric == BOLT_DOT;
+    // register list capacity: smallest of {4, 12, 16, 32} >= k (bubble cost ~ 2 KMAX)
+    if (k <= 4)
+        return dot ? launch_mk<M, true, 4>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 4>(a, k, index_base, rparts, part_keys, gthr, s);
+    if (k <= 12)
+        return dot ? launch_mk<M, true, 12>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 12>(a, k, index_base, rparts, part_keys, gthr, s);
     if (k <= 16)
-        return dot ? launch_mk<M, true, 16>(a, k, index_base, rparts, part_keys, s)
-                   : launch_mk<M, false, 16>(a, k, index_base, rparts, part_keys, s);
-    return dot ? launch_mk<M, true, 32>(a, k, index_base, rparts, part_keys, s)
-               : launch_mk<M, false, 32>(a, k, index_base, rparts, part_keys, s);
+        return dot ? launch_mk<M, true, 16>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 16>(a, k, index_base, rparts, part_keys, gthr, s);
+    return dot ? launch_mk<M, true, 32>(a, k, index_base, rparts, part_keys, gthr, s)
+               : launch_mk<M, false, 32>(a, k, index_base, rparts, part_keys, gthr, s);
 }
 
 }  // namespace tc
@@ -390,25 +578,30 @@ int topk_tc_supported(int64_t n, int m, int64_t nq, int k) {
     return n >= 1 && k >= 1 && k <= tc::kMaxTopk && (m == 8 || m == 16 || m == 32);
 }
 
-// One CTA per SM; units = query tiles x row partitions, the partition count
-// chosen so the unit count fills whole waves of the SMs (>= 4 waves), with at
-// least 16 vector tiles per unit.
+// One CTA pair per two SMs; units = 256-query tiles x row partitions, the
+// partition count chosen so units fill whole waves of SM pairs (>= 4
+// waves), with at least 16 vector tiles per unit and each unit's range
+// within the epilogue's local index bits.  Two partial lists per unit (the
+// two column-half epilogue warps).
 int topk_tc_parts(int64_t n, int m, int64_t nq, int k, int num_sms) {
     (void)k;
-    const int64_t tiles_q = ceil_div(nq, tc::kQM);
-    const int N = m == 8 ? tc::Cfg<8>::N : (m == 16 ? tc::Cfg<16>::N : tc::Cfg<32>::N);
-    // two partial lists per row partition (the two column-half epilogue warps)
-    return 2 * choose_parts(tiles_q, ceil_div(n, 8), num_sms, (int64_t)N * 16 / 8);
+    const int64_t tiles_q = ceil_div(nq, 2 * tc::kQM);
+    const int64_t max_range = m == 8 ? tc::Cfg<8>::MAX_RANGE : (m == 16 ? tc::Cfg<16>::MAX_RANGE : tc::Cfg<32>::MAX_RANGE);
+    int rparts = choose_parts(tiles_q, ceil_div(n, 8), num_sms / 2, (int64_t)256 * 16 / 8);
+    rparts = (int)max64(rparts, ceil_div(n, max_range - 8));
+    return 2 * rparts;
 }
 
+// part_keys holds parts*nq*k keys followed by nq u32 shared thresholds.
 cudaError_t launch_topk_tc(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
                            uint64_t* part_keys, int sms, cudaStream_t s) {
     (void)sms;
     const int rparts = parts / 2;
+    uint32_t* gthr = reinterpret_cast<uint32_t*>(part_keys + (size_t)parts * a.nq * k);
     switch (a.m) {
-        case 8: return tc::launch_m<8>(a, k, metric, index_base, rparts, part_keys, s);
-        case 16: return tc::launch_m<16>(a, k, metric, index_base, rparts, part_keys, s);
-        case 32: return tc::launch_m<32>(a, k, metric, index_base, rparts, part_keys, s);
+        case 8: return tc::launch_m<8>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+        case 16: return tc::launch_m<16>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+        case 32: return tc::launch_m<32>(a, k, metric, index_base, rparts, part_keys, gthr, s);
         default: return cudaErrorInvalidValue;
     }
 }

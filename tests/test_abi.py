@@ -67,7 +67,8 @@ def test_host_validation(lib):
     assert lib.bolt_topk_ex(k, 10, 8, k, 4, 10, 2, 0, None, None, 0, 0, None) == E_RANGE
     assert lib.bolt_topk_ex(k, 10, 8, k, 4, 10, 0, 0, None, None, 0, 7, None) == E_RANGE
     assert lib.bolt_topk_ex(k, 10, 8, k, 4, 10, 0, 1 << 48, None, None, 0, 0, None) == E_RANGE
-    assert lib.bolt_topk_merge(None, 100, 4, 100, None, None) == E_SHAPE
+    assert lib.bolt_topk_merge(None, 20000, 4, 100, None, None) == E_SHAPE
+    assert lib.bolt_topk_merge(None, 2, 4, 129, None, None) == E_SHAPE
     assert set(STATUS) == set(range(8))
 
 
@@ -75,6 +76,9 @@ def test_workspace_sizing_host(lib):
     # the plan is a pure function of the shapes (and SM count): parts * nq * k * 8 bytes
     for n, m, nq, k in [(10, 8, 4, 10), (1_000_000, 16, 10_000, 10), (10**8, 16, 1, 100)]:
         ws = lib.bolt_topk_workspace_bytes_ex(n, m, nq, k, 1)
-        assert ws % (nq * k * 8) == 0
-        parts = ws // (nq * k * 8)
-        assert parts == 0 or 2 <= parts <= 8192 // k
+        rv, parts = ctypes.c_int(0), ctypes.c_int(0)
+        assert lib.bolt_topk_plan(n, m, nq, k, 1, ctypes.byref(rv), ctypes.byref(parts)) == 0
+        assert rv.value == 1
+        # partial lists [parts][nq][k] u64 + one u32 shared threshold per query
+        assert ws == (0 if parts.value == 1 else parts.value * nq * k * 8 + nq * 4)
+        assert 1 <= parts.value <= 16384

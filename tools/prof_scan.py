@@ -49,3 +49,18 @@ for _ in range(a.reps):
 e.record()
 torch.cuda.synchronize()
 print(f"{a.what} {a.variant} n={a.n} nq={a.nq} m={a.m}: {s.elapsed_time(e) / a.reps:.3f} ms")
+
+if os.environ.get("BOLT_COUNTERS"):
+    import ctypes
+    buf = (ctypes.c_uint64 * 16)()
+    bolt._lib.load().bolt_debug_counters(ctypes.cast(buf, ctypes.c_void_p), 16)
+    names = ["prod_wait_empty", "epi_wait_tfull", "epi_wait+load", "mma_wait_full", "mma_wait_tempty",
+             "tiles(leader)", "cta_cycles", "ctas", "epi_proc_cycles", "slow_entries", "inserts"]
+    tiles = max(buf[5], 1)
+    ctas = max(buf[7], 1)
+    print("counters:", {n: int(buf[i]) for i, n in enumerate(names)})
+    print(f"per tile: mma_wait_full={buf[3]/tiles:.0f} mma_wait_tempty={buf[4]/tiles:.0f} "
+          f"cta_cycles/tile={buf[6]/ctas/(tiles/(ctas/2)):.0f} prod_wait_empty/tile={buf[0]/(tiles*2):.0f} "
+          f"epi_wait_tfull/tile={buf[1]/(tiles*2):.0f} epi_wait+load/tile={buf[2]/(tiles*2):.0f} "
+          f"epi_proc/warp-tile={buf[8]/(tiles*16):.0f} slow/lane-chunk={buf[9]/(tiles*16*4*32):.4f} "
+          f"inserts/lane-chunk={buf[10]/(tiles*16*4*32):.4f}")
