@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--nq", type=int, default=0, help="override queries (debug)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-graph", action="store_true", help="time the step eagerly instead of a CUDA graph")
     return p.parse_args()
 
 
@@ -181,6 +182,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1706_10283_b200 as bolt
+    from paper_1706_10283_b200.dist import gather_keys
 
     rank, world, local = dist_env()
     if world != args.gpus:
@@ -216,26 +218,39 @@ def run_ours(args):
     ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
     gathered = torch.empty((world, nq, k), dtype=torch.uint64, device=dev) if world > 1 else None
     final = torch.empty((nq, k), dtype=torch.uint64, device=dev) if world > 1 else keys
-    stream = torch.cuda.current_stream(dev)
     ev_scan = []
 
-    def step(timed: bool):
+    def step():
         bolt.encode(Xd, model.C, out=codes)
         bolt.build_quantized_luts(Qd, model.C, metric, model.a, model.b, out=ql)
-        if timed:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
         bolt.topk(codes, n, ql, k, metric, index_base=rank * n, variant=variant, out=keys, workspace=ws)
-        if timed:
-            e1.record(stream)
-            ev_scan.append((e0, e1))
         if world > 1:
-            dist.all_gather_into_tensor(gathered, keys)
-            bolt.topk_merge(gathered, out=final)
+            bolt.topk_merge(gather_keys(keys), out=final)
 
     for _ in range(args.warmup):
-        step(False)
+        step()
     torch.cuda.synchronize()
+    # The single-GPU step is captured once into a CUDA graph (no host enqueue
+    # jitter inside the timed region); with NCCL in the step it runs eagerly.
+    graph, graph_note = None, "eager"
+    if world == 1 and not args.no_graph:
+        try:
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                step()
+            torch.cuda.current_stream(dev).wait_stream(side)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            graph, graph_note = g, "cuda-graph replay"
+        except Exception as e:  # pragma: no cover - capture unsupported
+            graph_note = f"eager (graph capture failed: {e})"[:200]
+    stream = torch.cuda.current_stream(dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -245,8 +260,19 @@ def run_ours(args):
     with clk:
         t_start.record(stream)
         for _ in range(args.steps):
-            step(True)
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
         t_end.record(stream)
+        torch.cuda.synchronize()
+        # dominant kernel alone (scan + fused top-k), CUDA events on its stream
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            bolt.topk(codes, n, ql, k, metric, index_base=rank * n, variant=variant, out=keys, workspace=ws)
+            e1.record(stream)
+            ev_scan.append((e0, e1))
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -274,8 +300,7 @@ def run_ours(args):
             hs(Xh, Qh, model.C, metric, model.a, model.b, kh)
             if world > 1:
                 kd.copy_(kh, non_blocking=True)
-                dist.all_gather_into_tensor(gathered, kd)
-                bolt.topk_merge(gathered, out=final)
+                bolt.topk_merge(gather_keys(kd), out=final)
                 kh.copy_(final, non_blocking=True)
 
         e2e_step()
@@ -313,7 +338,7 @@ def run_ours(args):
                                    f"Q={nq}, squared L2, top-{k}; step = encode + fp64 LUT build/quantize "
                                    f"+ scan/top-k" + (" + NCCL all-gather + merge" if world > 1 else ""),
                        "n_per_gpu": n, "nq": nq, "m": cfg.m, "j": cfg.j, "k": k,
-                       "variant": used_variant, "scan_parts": parts,
+                       "variant": used_variant, "scan_parts": parts, "timing": graph_note,
                        "l2": "inputs > L2: the 512 MB fp32 database is streamed by the encoder every step",
                        "parallelism": f"row-sharded dp{world}"},
             "roofline": roof,
