@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libbolt.so")
+# BOLT_LIB selects another in-tree build (tools/ use libbolt_prof.so)
+LIB_PATH = os.path.join(_PKG, os.environ.get("BOLT_LIB", "libbolt.so"))
 
 BOLT_OK = 0
 STATUS = {0: "BOLT_OK", 1: "BOLT_E_NULL", 2: "BOLT_E_SHAPE", 3: "BOLT_E_RANGE", 4: "BOLT_E_ALIGN",

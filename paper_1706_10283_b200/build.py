@@ -42,8 +42,8 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src, verbose):
-    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+def _compile(src, verbose, objdir=OBJ):
+    obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
     hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "bolt.h")]
     if not _stale(obj, [src] + hdrs):
         return obj, ""
@@ -56,34 +56,41 @@ def _compile(src, verbose):
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
-    """profile=True adds -DBOLT_PROFILE (cycle counters, tools/ only)."""
+def build(force: bool = False, verbose: bool = False, profile: bool = False, xmode: bool = False) -> str:
+    """Diagnostic builds (tools/ only, loaded with BOLT_LIB=<name>):
+    profile=True -> libbolt_prof.so with -DBOLT_PROFILE (cycle counters) and -DBOLT_XMODE;
+    xmode=True -> libbolt_x.so with -DBOLT_XMODE (BOLT_TC_XMODE experiment
+    switches that skip pipeline stages; results are wrong by design)."""
     global NVCC_FLAGS
+    lib, objdir = LIB, OBJ
     if profile:
-        NVCC_FLAGS = NVCC_FLAGS + ["-DBOLT_PROFILE"]
-        force = True
-    os.makedirs(OBJ, exist_ok=True)
-    if not force and not _stale(LIB, _deps()):
-        return LIB
+        NVCC_FLAGS = NVCC_FLAGS + ["-DBOLT_PROFILE", "-DBOLT_XMODE"]
+        lib, objdir = os.path.join(PKG, "libbolt_prof.so"), OBJ + "_prof"
+    elif xmode:
+        NVCC_FLAGS = NVCC_FLAGS + ["-DBOLT_XMODE"]
+        lib, objdir = os.path.join(PKG, "libbolt_x.so"), OBJ + "_x"
+    os.makedirs(objdir, exist_ok=True)
+    if not force and not _stale(lib, _deps()):
+        return lib
     if force:
-        for o in glob.glob(os.path.join(OBJ, "*.o")):
+        for o in glob.glob(os.path.join(objdir, "*.o")):
             os.remove(o)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        results = list(ex.map(lambda s: _compile(s, verbose), _sources()))
+        results = list(ex.map(lambda s: _compile(s, verbose, objdir), _sources()))
     if verbose:
         for _, log in results:
             if log:
                 sys.stderr.write(log)
     objs = [o for o, _ in results]
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv or "--profile" in sys.argv, verbose="--verbose" in sys.argv,
-                profile="--profile" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv,
+                profile="--profile" in sys.argv, xmode="--xmode" in sys.argv))

@@ -7,6 +7,8 @@
 
 #include <atomic>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 using namespace bolt;
@@ -85,10 +87,26 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // ---- top-k plan shared by workspace sizing and execution
 struct TopkPlan {
-    int variant;   // resolved PRMT / TC
+    int variant;     // resolved PRMT / TC
     int parts;
+    int64_t pre_n;   // TC: rows of the threshold-seeding prefix pass (0 = none)
+    int pre_parts;
     size_t ws;
+    size_t pre_off;  // byte offset of the prefix pass's partial lists + thresholds in ws
 };
+
+
+// Rows of the prefix sample that seeds the tcgen05 scan's shared thresholds
+// (scan_tc.cu): its exact top-k gives, per query, a value that at least k
+// database rows reach, so the full scan never has to fill its lists from
+// scratch.  Used when the database is >= 32x the sample.
+int64_t tc_prefix_rows(int64_t n) {
+    int64_t rows = 0;  // off: measured no net gain on c2 (profiles/r1); kept for sweeps
+#ifdef BOLT_XMODE
+    if (const char* e = getenv("BOLT_TC_PREFIX")) rows = atoll(e);  // diagnostic sweeps (tools/)
+#endif
+    return rows > 0 && n >= 32 * rows ? rows : 0;
+}
 
 TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     TopkPlan p{};
@@ -99,6 +117,15 @@ TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     p.ws = p.parts > 1 ? (size_t)p.parts * nq * k * sizeof(uint64_t) : 0;
     // both variants keep a per-query shared threshold array (u32) after the partial lists
     if (p.ws > 0) p.ws += (size_t)nq * sizeof(uint32_t);
+    if (v == BOLT_VARIANT_TC && p.parts > 1) {
+        p.pre_n = tc_prefix_rows(n);
+        if (p.pre_n > 0) {
+            p.pre_parts = topk_tc_parts(p.pre_n, m, nq, k, sms);
+            if (p.pre_parts > 32) p.pre_parts = 32;
+            p.pre_off = align256(p.ws);
+            p.ws = p.pre_off + (size_t)p.pre_parts * nq * k * sizeof(uint64_t) + (size_t)nq * sizeof(uint32_t);
+        }
+    }
     return p;
 }
 
@@ -297,9 +324,21 @@ bolt_status bolt_topk_ex(const uint32_t* codes, int64_t n, int m, const uint8_t*
     if (p.ws > 0 && !aligned(ws, 8)) return fail(BOLT_E_ALIGN, "workspace must be 8-byte aligned");
     ScanArgs a{codes, n, ceil_div(n, 8), m, qluts, nq};
     uint64_t* parts_out = p.parts > 1 ? static_cast<uint64_t*>(ws) : out_keys;
-    cudaError_t e = p.variant == BOLT_VARIANT_TC
-                        ? launch_topk_tc(a, k, metric, index_base, p.parts, parts_out, d.sms, s)
-                        : launch_topk_prmt(a, k, metric, index_base, p.parts, parts_out, d.sms, s);
+    cudaError_t e = cudaSuccess;
+    if (p.variant == BOLT_VARIANT_TC && p.pre_n > 0) {
+        // threshold seed: exact top-k of the first pre_n rows -> shared thresholds of the full scan
+        uint64_t* pre_keys = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(ws) + p.pre_off);
+        ScanArgs pa{codes, p.pre_n, ceil_div(p.pre_n, 8), m, qluts, nq};
+        e = launch_topk_tc(pa, k, metric, 0, p.pre_parts, pre_keys, d.sms, s, true);
+        if (e != cudaSuccess) return cuda_status(e, "bolt_topk prefix scan");
+        uint32_t* gthr = reinterpret_cast<uint32_t*>(parts_out + (size_t)p.parts * nq * k);
+        e = launch_prefix_threshold(pre_keys, p.pre_parts, nq, k, metric, 255u * (uint32_t)m, gthr, s);
+        if (e != cudaSuccess) return cuda_status(e, "bolt_topk prefix threshold");
+        e = launch_topk_tc(a, k, metric, index_base, p.parts, parts_out, d.sms, s, false);
+    } else {
+        e = p.variant == BOLT_VARIANT_TC ? launch_topk_tc(a, k, metric, index_base, p.parts, parts_out, d.sms, s)
+                                         : launch_topk_prmt(a, k, metric, index_base, p.parts, parts_out, d.sms, s);
+    }
     if (e != cudaSuccess) return cuda_status(e, "bolt_topk scan");
     if (p.parts > 1) return cuda_status(launch_merge(parts_out, p.parts, nq, k, out_keys, s), "bolt_topk merge");
     return BOLT_OK;

@@ -59,13 +59,22 @@ inline int choose_parts(int64_t tiles, int64_t groups, int64_t W, int64_t min_gr
 }
 
 // Diagnostic cycle counters (BOLT_PROFILE builds only).
-constexpr int kNumCounters = 16;
+constexpr int kNumCounters = 24;
 #ifdef BOLT_PROFILE
 // defined (per translation unit that uses it) by BOLT_DEFINE_COUNTERS
 #define BOLT_PROF_ADD(i, v) atomicAdd(&g_counters[(i)], (unsigned long long)(v))
+// warp-aggregated: one atomic per group of converged lanes; `lanes` != 0 adds
+// the number of active lanes, else 1 per warp group
+#define BOLT_PROF_WARP(i, lanes)                                                               \
+    do {                                                                                       \
+        const unsigned _am = __activemask();                                                   \
+        if ((threadIdx.x & 31) == (unsigned)(__ffs(_am) - 1))                                  \
+            atomicAdd(&g_counters[(i)], (unsigned long long)((lanes) ? __popc(_am) : 1));      \
+    } while (0)
 #define BOLT_CLOCK() clock64()
 #else
 #define BOLT_PROF_ADD(i, v) ((void)0)
+#define BOLT_PROF_WARP(i, lanes) ((void)0)
 #define BOLT_CLOCK() 0ll
 #endif
 
@@ -106,8 +115,12 @@ cudaError_t launch_topk_prmt(const ScanArgs& a, int k, int metric, int64_t index
 // top-k (tcgen05 variant)
 int topk_tc_supported(int64_t n, int m, int64_t nq, int k);
 int topk_tc_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
+// part_keys: parts*nq*k keys followed by nq u32 shared thresholds (zeroed
+// by the launch when init_thresholds, else seeded by the caller)
 cudaError_t launch_topk_tc(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
-                           uint64_t* part_keys, int sms, cudaStream_t s);
+                           uint64_t* part_keys, int sms, cudaStream_t s, bool init_thresholds = true);
+cudaError_t launch_prefix_threshold(const uint64_t* keys, int w, int64_t nq, int k, int metric, uint32_t kvmax,
+                                    uint32_t* gthr, cudaStream_t s);
 constexpr int kMaxParts = 16384;  // merge limit (shared memory of the tournament merge)
 
 int tc_debug_counters(uint64_t* out, int n);  // scan_tc.cu (BOLT_PROFILE builds)

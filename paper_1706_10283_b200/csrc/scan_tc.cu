@@ -29,6 +29,8 @@
 // Shared-memory operand layout (both K-major, SWIZZLE_NONE): the 16-byte
 // chunk j of row r lives at j * (rows * 16) + (r / 8) * 128 + (r % 8) * 16,
 // so SBO (next 8 rows) = 128 B and LBO (next 16-byte K chunk) = rows * 16 B.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "topk_list.cuh"
 
@@ -232,6 +234,13 @@ struct RegList {
     __device__ __forceinline__ uint32_t threshold(int idx_bits) const {
         return v[KMAX - 1] == 0xFFFFFFFFu ? kNotFull : (v[KMAX - 1] >> idx_bits);
     }
+    // value of the entry in slot `pos` (kNotFull if empty); select chain, no local memory
+    __device__ __forceinline__ uint32_t value_at(int pos, int idx_bits) const {
+        uint32_t r = 0xFFFFFFFFu;
+#pragma unroll
+        for (int i = 0; i < KMAX; ++i) r = i == pos ? v[i] : r;
+        return r == 0xFFFFFFFFu ? kNotFull : (r >> idx_bits);
+    }
 };
 
 }  // namespace tc
@@ -260,7 +269,10 @@ __device__ __forceinline__ uint32_t candidate_mask(const uint32_t (&p)[16], uint
 template <int M, bool kDot, int KMAX>
 __global__ void __launch_bounds__(kThreads, 1)
 topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, uint64_t* __restrict__ part_keys,
-               uint32_t* __restrict__ gthr_inv) {
+               uint32_t* __restrict__ gthr_inv, int xmode) {
+#ifndef BOLT_XMODE
+    xmode = 0;  // diagnostic stage switches exist only in libbolt_x.so (tools/)
+#endif
     using C = Cfg<M>;
     constexpr int S = C::STAGES;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -343,7 +355,9 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             const int v = t;                                               // NH == kProducers
             const uint32_t* wv = cst + (v >> 3) * M;
             const uint32_t sh = (v & 7) * 4;
-            if (hb + C::NH <= vend) {
+            if (xmode & 2) {
+                // diagnostic: keep the stage's stale one-hot rows
+            } else if (hb + C::NH <= vend) {
 #pragma unroll
                 for (int c4 = 0; c4 < M; c4 += 4) {
                     const uint4 w = *reinterpret_cast<const uint4*>(wv + c4);
@@ -385,7 +399,8 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
         const bool qvalid = q0 + q < a.nq;
         uint32_t* gq = gthr_inv + (qvalid ? q0 + q : 0);
         uint32_t thr = kNotFull;
-        uint32_t g_next = 0;  // inverted shared threshold (0 = none yet)
+        uint32_t g_next;  // inverted shared threshold (0 = none yet), fetched a tile ahead
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g_next) : "l"(gq));
         const uint32_t tlane = (uint32_t)(quad * 32) << 16;
         for (int tile = 0; tile < ntiles; ++tile) {
             const int d = tile & 1;
@@ -397,10 +412,17 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             // release the accumulator at once, so that a slow filter pass on
             // this warp never holds the MMA back
             uint32_t p[4][16];
+            if (xmode & 8) {  // diagnostic: no TMEM reads
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) p[c][i] = 0xFFFFFFFFu;
+            } else {
 #pragma unroll
             for (int c = 0; c < 4; ++c)
                 tmem_ld16p(tmem + tlane + (uint32_t)(d * C::N + half * kCols + c * 32), p[c]);
             tmem_wait_ld();
+            }
             if (threadIdx.x == 128) BOLT_PROF_ADD(2, BOLT_CLOCK() - tw0);  // wait + TMEM load
             tc_fence_before();
             __syncwarp();
@@ -409,8 +431,11 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                 else mbar_arrive_cluster(&tempty[d], 0);
             }
             const long long tp0 = BOLT_CLOCK();
+            if (xmode & 1) continue;  // diagnostic: load + release only
             // shared threshold: use the value fetched one tile ago, prefetch the next
             thr = min(own, 0xFFFFu - g_next + 1u);
+            if (tile >= 1 && thr > 0xFFFFu) BOLT_PROF_WARP(17, 1);  // lanes without a threshold after tile 0
+            if (tile == 1) BOLT_PROF_ADD(18, thr);
             asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g_next) : "l"(gq));
             const int tbl = tile * C::N;  // local index of the tile's first vector
             const int nvalid = (int)min64(C::N, vend - vbeg - tbl);
@@ -433,6 +458,10 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             const uint32_t best = kDot ? max(u & 0xFFFFu, u >> 16) : min(u & 0xFFFFu, u >> 16);
             const uint32_t kvbest = kDot ? C::KVMAX - best : best;
             const bool tail = nvalid < C::N;
+            if (xmode & 4) {  // diagnostic: filter only, never the slow path
+                if (kvbest == 0xFFFFFFFFu) list.insert(kvbest);
+                continue;
+            }
             if (kvbest < thr || tail) {
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -440,7 +469,9 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                     const uint32_t cbest = kDot ? max(cb[c] & 0xFFFFu, cb[c] >> 16) : min(cb[c] & 0xFFFFu, cb[c] >> 16);
                     const int nleft = nvalid - col;
                     if ((kDot ? C::KVMAX - cbest : cbest) >= thr && nleft >= 32) continue;
-                    BOLT_PROF_ADD(9, 1);  // lane slow-path entries
+                    BOLT_PROF_WARP(9, 1);   // lane slow-path entries
+                    BOLT_PROF_WARP(11, 0);  // warp-chunk slow-path entries
+                    BOLT_PROF_WARP(tile < 8 ? 12 : tile < 64 ? 13 : tile < 256 ? 14 : 15, 0);  // ... by tile index
                     // slow path (lane-divergent): candidate mask, values parked in
                     // this thread's scratch row, per-lane loop over its candidates
                     uint32_t mask = thr == kNotFull ? 0xFFFFFFFFu
@@ -450,6 +481,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                     for (int i = 0; i < 4; ++i)
                         sv[i] = make_uint4(p[c][4 * i], p[c][4 * i + 1], p[c][4 * i + 2], p[c][4 * i + 3]);
                     while (mask) {
+                        BOLT_PROF_WARP(16, 0);  // warp iterations of the candidate loop
                         const int bpos = __ffs(mask) - 1;
                         mask &= mask - 1;
                         const int j = 4 * (bpos & 7) + (bpos >> 3);
@@ -459,7 +491,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                             list.insert((kv << C::IDX_BITS) | (uint32_t)(tbl + col + j));
                             own = list.threshold(C::IDX_BITS);
                             thr = min(thr, own);
-                            BOLT_PROF_ADD(10, 1);  // inserts
+                            BOLT_PROF_WARP(10, 1);  // inserts
                         }
                     }
                 }
@@ -530,7 +562,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
 
 template <int M, bool kDot, int KMAX>
 cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, uint64_t* part_keys,
-                      uint32_t* gthr, cudaStream_t s) {
+                      uint32_t* gthr, cudaStream_t s, bool init_thr) {
     using C = Cfg<M>;
     const int tiles_q = (int)ceil_div(a.nq, 2 * kQM);
     const int64_t vpp = ceil_div(ceil_div(a.n, rparts), 8) * 8;
@@ -548,27 +580,33 @@ cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)a.nq * sizeof(uint32_t), s);
-    if (e != cudaSuccess) return e;
-    return cudaLaunchKernelEx(&cfg, kern, a, k, index_base, vpp, tiles_q, part_keys, gthr);
+    int xmode = 0;
+#ifdef BOLT_XMODE
+    if (const char* x = getenv("BOLT_TC_XMODE")) xmode = atoi(x);
+#endif
+    if (init_thr && !(xmode & 16)) {  // diagnostic 16: keep caller-prefilled shared thresholds
+        cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)a.nq * sizeof(uint32_t), s);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaLaunchKernelEx(&cfg, kern, a, k, index_base, vpp, tiles_q, part_keys, gthr, xmode);
 }
 
 template <int M>
 cudaError_t launch_m(const ScanArgs& a, int k, int metric, int64_t index_base, int rparts, uint64_t* part_keys,
-                     uint32_t* gthr, cudaStream_t s) {
+                     uint32_t* gthr, cudaStream_t s, bool it) {
     const bool dot = metric == BOLT_DOT;
     // register list capacity: smallest of {4, 12, 16, 32} >= k (bubble cost ~ 2 KMAX)
     if (k <= 4)
-        return dot ? launch_mk<M, true, 4>(a, k, index_base, rparts, part_keys, gthr, s)
-                   : launch_mk<M, false, 4>(a, k, index_base, rparts, part_keys, gthr, s);
+        return dot ? launch_mk<M, true, 4>(a, k, index_base, rparts, part_keys, gthr, s, it)
+                   : launch_mk<M, false, 4>(a, k, index_base, rparts, part_keys, gthr, s, it);
     if (k <= 12)
-        return dot ? launch_mk<M, true, 12>(a, k, index_base, rparts, part_keys, gthr, s)
-                   : launch_mk<M, false, 12>(a, k, index_base, rparts, part_keys, gthr, s);
+        return dot ? launch_mk<M, true, 12>(a, k, index_base, rparts, part_keys, gthr, s, it)
+                   : launch_mk<M, false, 12>(a, k, index_base, rparts, part_keys, gthr, s, it);
     if (k <= 16)
-        return dot ? launch_mk<M, true, 16>(a, k, index_base, rparts, part_keys, gthr, s)
-                   : launch_mk<M, false, 16>(a, k, index_base, rparts, part_keys, gthr, s);
-    return dot ? launch_mk<M, true, 32>(a, k, index_base, rparts, part_keys, gthr, s)
-               : launch_mk<M, false, 32>(a, k, index_base, rparts, part_keys, gthr, s);
+        return dot ? launch_mk<M, true, 16>(a, k, index_base, rparts, part_keys, gthr, s, it)
+                   : launch_mk<M, false, 16>(a, k, index_base, rparts, part_keys, gthr, s, it);
+    return dot ? launch_mk<M, true, 32>(a, k, index_base, rparts, part_keys, gthr, s, it)
+               : launch_mk<M, false, 32>(a, k, index_base, rparts, part_keys, gthr, s, it);
 }
 
 }  // namespace tc
@@ -594,14 +632,14 @@ int topk_tc_parts(int64_t n, int m, int64_t nq, int k, int num_sms) {
 
 // part_keys holds parts*nq*k keys followed by nq u32 shared thresholds.
 cudaError_t launch_topk_tc(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
-                           uint64_t* part_keys, int sms, cudaStream_t s) {
+                           uint64_t* part_keys, int sms, cudaStream_t s, bool init_thresholds) {
     (void)sms;
     const int rparts = parts / 2;
     uint32_t* gthr = reinterpret_cast<uint32_t*>(part_keys + (size_t)parts * a.nq * k);
     switch (a.m) {
-        case 8: return tc::launch_m<8>(a, k, metric, index_base, rparts, part_keys, gthr, s);
-        case 16: return tc::launch_m<16>(a, k, metric, index_base, rparts, part_keys, gthr, s);
-        case 32: return tc::launch_m<32>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+        case 8: return tc::launch_m<8>(a, k, metric, index_base, rparts, part_keys, gthr, s, init_thresholds);
+        case 16: return tc::launch_m<16>(a, k, metric, index_base, rparts, part_keys, gthr, s, init_thresholds);
+        case 32: return tc::launch_m<32>(a, k, metric, index_base, rparts, part_keys, gthr, s, init_thresholds);
         default: return cudaErrorInvalidValue;
     }
 }

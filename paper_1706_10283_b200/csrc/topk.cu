@@ -76,7 +76,49 @@ __global__ void keys_split_kernel(const uint64_t* __restrict__ keys, int64_t cou
     if (idx) idx[e] = (int64_t)(key & ((1ull << 48) - 1));
 }
 
+// Shared-threshold seed from a prefix sample (scan_tc.cu): per query the k-th
+// smallest key of the union of w sorted partial lists over the sample rows,
+// converted to the tcgen05 epilogue's inverted threshold 0xFFFF - kv'
+// (kv' = acc for L2, 255 M - acc for dot).  Every row of the sample is a row
+// of the database, so at least k keys of the full top-k search have a value
+// <= that one: a valid bound for the full scan (0 = no bound if the sample
+// holds fewer than k keys).
+__global__ void prefix_threshold_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int k, int metric,
+                                        uint32_t kvmax, uint32_t* __restrict__ gthr) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    int pos[32];
+    for (int p = 0; p < w; ++p) pos[p] = 0;
+    uint64_t kth = ~0ull;
+    for (int r = 0; r < k; ++r) {
+        uint64_t best = ~0ull;
+        int bi = -1;
+        for (int p = 0; p < w; ++p) {
+            const uint64_t h = pos[p] < k ? keys[((int64_t)p * nq + q) * k + pos[p]] : ~0ull;
+            if (h < best) { best = h; bi = p; }
+        }
+        if (bi < 0) break;
+        ++pos[bi];
+        kth = best;
+    }
+    uint32_t g = 0;
+    if (kth != ~0ull) {
+        const uint32_t v = (uint32_t)(kth >> 48);
+        const uint32_t kvp = metric == BOLT_DOT ? kvmax - (0xFFFFu - v) : v;
+        g = 0xFFFFu - kvp;
+    }
+    gthr[q] = g;
+}
+
 }  // namespace
+
+cudaError_t launch_prefix_threshold(const uint64_t* keys, int w, int64_t nq, int k, int metric, uint32_t kvmax,
+                                    uint32_t* gthr, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    if (w > 32) return cudaErrorInvalidValue;
+    prefix_threshold_kernel<<<(unsigned)ceil_div(nq, 128), 128, 0, s>>>(keys, w, nq, k, metric, kvmax, gthr);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_merge(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out,
                          cudaStream_t s) {
