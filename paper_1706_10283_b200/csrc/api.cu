@@ -135,7 +135,7 @@ extern "C" {
 
 int bolt_debug_counters(uint64_t* out, int n) {
     if (!out || n <= 0) return 0;
-    return tc_debug_counters(out, n < kNumCounters ? n : kNumCounters);
+    return tc_debug_counters(out, n);  // counters, then (libbolt_x.so) the scan trace
 }
 
 const char* bolt_version(void) { return "bolt-b200 1.0 (abi 1, sm_100a)"; }

@@ -39,28 +39,55 @@ namespace bolt {
 __device__ unsigned long long g_counters[kNumCounters];
 #endif
 
+#ifdef BOLT_XMODE
+// per-tile clock64 timeline of CTA 0 (BOLT_TC_XMODE & 64; tools/ only)
+// [rank][tile][col] for the two CTAs of cluster 0
+constexpr int kTraceTiles = 512, kTraceCols = 40;
+__device__ unsigned long long g_trace[2 * kTraceTiles * kTraceCols];
+#define BOLT_TRACE(tile, col)                                                               \
+    do {                                                                                    \
+        if ((xmode & 64) && blockIdx.x < 2 && (tile) < kTraceTiles)                         \
+            g_trace[(blockIdx.x * kTraceTiles + (tile)) * kTraceCols + (col)] = clock64();  \
+    } while (0)
+#else
+#define BOLT_TRACE(tile, col) ((void)0)
+#endif
+
 int tc_debug_counters(uint64_t* out, int n) {
+    const int nc = n < kNumCounters ? n : kNumCounters;
 #ifdef BOLT_PROFILE
     unsigned long long h[kNumCounters] = {};
     cudaMemcpyFromSymbol(h, g_counters, sizeof(h));
     unsigned long long z[kNumCounters] = {};
     cudaMemcpyToSymbol(g_counters, z, sizeof(z));
-    for (int i = 0; i < n; ++i) out[i] = h[i];
+    for (int i = 0; i < nc; ++i) out[i] = h[i];
 #else
-    for (int i = 0; i < n; ++i) out[i] = 0;
+    for (int i = 0; i < nc; ++i) out[i] = 0;
 #endif
-    return n;
+    if (n <= kNumCounters) return nc;
+#ifdef BOLT_XMODE
+    const int nt = n - kNumCounters < 2 * kTraceTiles * kTraceCols ? n - kNumCounters : 2 * kTraceTiles * kTraceCols;
+    cudaMemcpyFromSymbol(out + kNumCounters, g_trace, nt * sizeof(uint64_t));
+    return kNumCounters + nt;
+#else
+    return nc;
+#endif
 }
 
 namespace tc {
 
 constexpr int kQM = 128;                 // queries per CTA = TMEM lanes (MMA M = 256 per pair)
-constexpr int kProducers = 128;
+constexpr int kProdWarps = 4;            // thread = vector (NH = 128 per CTA)
+constexpr int kProducers = kProdWarps * 32;
 constexpr int kEpiWarps = 8;             // two warps per TMEM lane quadrant (column halves)
 constexpr int kEpilogue = kEpiWarps * 32;
-constexpr int kMmaWarp = 4 + kEpiWarps;
-constexpr int kThreads = (kMmaWarp + 1) * 32;  // 4 producer + 8 epilogue + 1 MMA warp
+constexpr int kMmaWarp = kProdWarps + kEpiWarps;
+// Warp roles by index: epilogue 0-7, producers 8-11, MMA issuer 12.  The
+// SMSP schedulers favour higher warp ids, so the producers, whose one-hot
+// stages gate the MMA, win issue slots over the epilogue's filter work.
+constexpr int kThreads = (kMmaWarp + 1) * 32;
 constexpr int kMaxTopk = 32;
+constexpr int kPrefetch = 3;             // tiles of code words in flight per producer thread
 constexpr int kScratchStride = 20;       // u32 words per epilogue thread: 32 u16 values + pad
 
 template <int M>
@@ -71,8 +98,8 @@ struct Cfg {
     static constexpr int A_BYTES = kQM * K;
     static constexpr int B_BYTES = NH * K;                // one stage of this CTA's half of B
     static constexpr int SCRATCH_BYTES = kEpilogue * kScratchStride * 4;
-    static constexpr int STAGES_RAW = (220 * 1024 - A_BYTES - SCRATCH_BYTES) / (B_BYTES + NH * M / 2);
-    static constexpr int STAGES = STAGES_RAW > 4 ? 4 : STAGES_RAW;
+    static constexpr int STAGES_RAW = (220 * 1024 - A_BYTES - SCRATCH_BYTES) / B_BYTES;
+    static constexpr int STAGES = STAGES_RAW > 5 ? 5 : STAGES_RAW;
     static_assert(STAGES >= 2, "shared memory too small for a double-buffered B tile");
     static constexpr int KSTEPS = K / 32;
     static constexpr int TMEM_COLS = 512;                  // 2 x 256-column accumulators
@@ -81,9 +108,8 @@ struct Cfg {
     static constexpr int IDX_BITS = 31 - VAL_BITS;
     static constexpr int64_t MAX_RANGE = int64_t(1) << IDX_BITS;
     static constexpr uint32_t KVMAX = 255u * M;
-    // dynamic smem: A | B[STAGES] | code stages [STAGES][NH*M/8] u32 | scratch | barriers
-    static constexpr int CODE_OFF = A_BYTES + STAGES * B_BYTES;
-    static constexpr int SCRATCH_OFF = CODE_OFF + STAGES * NH * M / 2;
+    // dynamic smem: A | B[STAGES] | scratch | barriers
+    static constexpr int SCRATCH_OFF = A_BYTES + STAGES * B_BYTES;
     static constexpr int BAR_OFF = SCRATCH_OFF + SCRATCH_BYTES;
     static constexpr int SMEM = BAR_OFF + 256;
     // instruction descriptor: D s32 (bits 4-5 = 2), A/B u8 (format 0), K-major,
@@ -121,6 +147,29 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // arrive on the mbarrier at the same shared-memory offset in CTA `cta` of the cluster
+// relaxed remote arrive: for the accumulator release, whose ordering comes
+// from tcgen05.wait::ld (the reads are complete), so the arrive need not wait
+// for this thread's outstanding global memory operations
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint64_t* bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 remote;\n\t"
+        "mapa.shared::cluster.u32 remote, %0, %1;\n\t"
+        "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [remote];\n\t}" ::"r"(smem_u32(bar)),
+        "r"(cta)
+        : "memory");
+}
+// remote arrive with the default .release.cta semantics (as CUTLASS's
+// ClusterBarrier::arrive(cta_id)): orders this thread's shared-memory
+// writes (after fence.proxy.async) without a cluster-scope fence that would
+// wait for its outstanding global loads
+__device__ __forceinline__ void mbar_arrive_remote_cta(uint64_t* bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 remote;\n\t"
+        "mapa.shared::cluster.u32 remote, %0, %1;\n\t"
+        "mbarrier.arrive.shared::cluster.b64 _, [remote];\n\t}" ::"r"(smem_u32(bar)),
+        "r"(cta)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
     asm volatile(
         "{\n\t.reg .b32 remote;\n\t"
@@ -278,7 +327,6 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sA = smem;
     uint8_t* sB = smem + C::A_BYTES;
-    uint32_t* codes_st = reinterpret_cast<uint32_t*>(smem + C::CODE_OFF);
     uint32_t* scratch_all = reinterpret_cast<uint32_t*>(smem + C::SCRATCH_OFF);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
     uint64_t* full = bars;                 // [S]  leader: producers of both CTAs -> MMA
@@ -300,7 +348,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
-            mbar_init(&full[i], 2);    // one arrive per CTA (after a producer named barrier)
+            mbar_init(&full[i], 2 * kProdWarps);  // one arrive per producer warp of both CTAs
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -321,9 +369,9 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
     const uint32_t tmem = *tmem_slot;
     const long long tk0 = BOLT_CLOCK();
 
-    if (warp < 4) {
+    if (warp >= kEpiWarps && warp < kMmaWarp) {
         // ------------------------------------------------------ producers
-        const int t = threadIdx.x;
+        const int t = threadIdx.x - kEpilogue;
         // A: this CTA's 128 queries, 16-byte unit (c, q) -> c*(128*16) + (q/8)*128 + (q%8)*16
         for (int u = t; u < kQM * M; u += kProducers) {
             const int c = u / kQM, q = u % kQM;
@@ -331,63 +379,87 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             if (q0 + q < a.nq) v = __ldg(reinterpret_cast<const uint4*>(a.qluts + ((q0 + q) * M + c) * kK));
             *reinterpret_cast<uint4*>(sA + c * (kQM * 16) + (q >> 3) * 128 + (q & 7) * 16) = v;
         }
-        // codes of this CTA's half tile = NH/8 groups x M words, contiguous
-        constexpr int kChunks = C::NH * M / 32;  // uint4 per half tile (<= 128)
-        static_assert(kChunks <= kProducers, "half-tile code block must fit one uint4 per producer");
-        const int64_t words_total = a.groups * M;
-        auto load_chunk = [&](int tile) -> uint4 {
-            const int64_t w0 = ((vbeg + (int64_t)tile * C::N + rank * C::NH) >> 3) * M + (int64_t)t * 4;
-            if (t < kChunks && w0 < words_total) return __ldg(reinterpret_cast<const uint4*>(a.codes + w0));
-            return make_uint4(0, 0, 0, 0);
+        // Thread t expands vector v = t of each tile: its M code words (the
+        // same for the 8 vectors of a layout-v1 group, one broadcast load)
+        // are fetched from global memory a tile ahead, so no producer barrier
+        // is needed; each warp arrives on the stage's full barrier on its own.
+        static_assert(C::NH == kProducers, "one producer thread per vector");
+        constexpr int MH = M;                       // codebooks per producer thread
+        constexpr int NW4 = MH / 4;                 // uint4 loads per thread
+        const int v = t;
+        constexpr int ch = 0;
+        const uint32_t sh = (v & 7) * 4;
+        auto load_words = [&](int tile, uint4 (&w)[NW4]) {
+            const int64_t g = (vbeg + (int64_t)tile * C::N + rank * C::NH + v) >> 3;
+#pragma unroll
+            for (int i = 0; i < NW4; ++i)
+                w[i] = g < a.groups ? __ldg(reinterpret_cast<const uint4*>(a.codes + g * M + ch * MH) + i)
+                                    : make_uint4(0, 0, 0, 0);
         };
-        uint4 pre = ntiles > 0 ? load_chunk(0) : make_uint4(0, 0, 0, 0);
-        for (int tile = 0; tile < ntiles; ++tile) {
+        // one tile of expansion: wait for the stage, write the one-hot rows,
+        // publish them to the async proxy and arrive on the stage's full barrier
+        auto produce = [&](int tile, const uint4 (&cur)[NW4]) {
             const int s = tile % S;
             long long tw0 = BOLT_CLOCK();
             mbar_wait(&empty[s], ((tile / S) & 1) ^ 1);
+            if (lane == 0) BOLT_TRACE(tile, 3 + t / 32);
             if (t == 0) BOLT_PROF_ADD(0, BOLT_CLOCK() - tw0);  // producer waits on empty
-            uint32_t* cst = codes_st + s * (C::NH * M / 8);
-            if (t < kChunks) reinterpret_cast<uint4*>(cst)[t] = pre;
-            asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");
-            if (tile + 1 < ntiles) pre = load_chunk(tile + 1);
-            uint8_t* b = sB + s * C::B_BYTES;
+            uint8_t* b = sB + s * C::B_BYTES + ch * MH * (C::NH * 16) + v * 16;
             const int64_t hb = vbeg + (int64_t)tile * C::N + rank * C::NH;  // first vector of this half
-            const int v = t;                                               // NH == kProducers
-            const uint32_t* wv = cst + (v >> 3) * M;
-            const uint32_t sh = (v & 7) * 4;
             if (xmode & 2) {
                 // diagnostic: keep the stage's stale one-hot rows
             } else if (hb + C::NH <= vend) {
 #pragma unroll
-                for (int c4 = 0; c4 < M; c4 += 4) {
-                    const uint4 w = *reinterpret_cast<const uint4*>(wv + c4);
-                    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+                for (int i = 0; i < NW4; ++i) {
+                    const uint32_t ws[4] = {cur[i].x, cur[i].y, cur[i].z, cur[i].w};
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        *reinterpret_cast<uint4*>(b + (c4 + j) * (C::NH * 16) + v * 16) =
+                    for (int j = 0; j < 4 && 4 * i + j < MH; ++j)
+                        *reinterpret_cast<uint4*>(b + (4 * i + j) * (C::NH * 16)) =
                             one_hot16_s(((ws[j] >> sh) & 0xFu) * 8u);
                 }
             } else {  // last, partial tile: rows past the range are all-zero
                 const bool valid = hb + v < vend;
-#pragma unroll 1
-                for (int c = 0; c < M; ++c)
-                    *reinterpret_cast<uint4*>(b + c * (C::NH * 16) + v * 16) =
-                        one_hot16_s(valid ? ((wv[c] >> sh) & 0xFu) * 8u : 128u);
+#pragma unroll
+                for (int i = 0; i < NW4; ++i) {
+                    const uint32_t ws[4] = {cur[i].x, cur[i].y, cur[i].z, cur[i].w};
+#pragma unroll
+                    for (int j = 0; j < 4 && 4 * i + j < MH; ++j)
+                        *reinterpret_cast<uint4*>(b + (4 * i + j) * (C::NH * 16)) =
+                            one_hot16_s(valid ? ((ws[j] >> sh) & 0xFu) * 8u : 128u);
+                }
             }
             fence_proxy_async();
-            asm volatile("bar.sync 2, %0;" ::"n"(kProducers) : "memory");
-            if (t == 0) {
+            __syncwarp();
+            if (lane == 0) {
+                BOLT_TRACE(tile, 7 + t / 32);
                 if (rank == 0) mbar_arrive(&full[s]);
-                else mbar_arrive_cluster(&full[s], 0);
+                else mbar_arrive_remote_cta(&full[s], 0);
+            }
+        };
+        // code words prefetched kPrefetch tiles ahead (a register ring indexed
+        // statically by unrolling the tile loop), issued after each arrive
+        constexpr int D = kPrefetch;
+        uint4 pre[D][NW4];
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            if (j < ntiles) load_words(j, pre[j]);
+        for (int t0 = 0; t0 < ntiles; t0 += D) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const int tile = t0 + j;
+                if (tile < ntiles) {
+                    produce(tile, pre[j]);
+                    if (tile + D < ntiles) load_words(tile + D, pre[j]);
+                }
             }
         }
-    } else if (warp < 4 + kEpiWarps) {
+    } else if (warp < kEpiWarps) {
         // ------------------------------------------------------- epilogue
         const int quad = warp & 3;                 // TMEM lanes 32*quad .. (warp % 4 rule)
-        const int half = (warp - 4) >> 2;          // column half of the tile
+        const int half = warp >> 2;                // column half of the tile
         const int q = quad * 32 + lane;            // query row of this CTA
         constexpr int kCols = C::N / 2;
-        uint32_t* scratch = scratch_all + (threadIdx.x - 128) * kScratchStride;
+        uint32_t* scratch = scratch_all + threadIdx.x * kScratchStride;
         RegList<KMAX> list;
         list.init(k);
         // Thresholds in kv' units.  own = k-th key of this list; shared =
@@ -406,7 +478,8 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             const int d = tile & 1;
             long long tw0 = BOLT_CLOCK();
             mbar_wait(&tfull[d], (tile >> 1) & 1);
-            if (threadIdx.x == 128) BOLT_PROF_ADD(1, BOLT_CLOCK() - tw0);  // epilogue waits on tfull
+            if (lane == 0) BOLT_TRACE(tile, 11 + warp);
+            if (threadIdx.x == 0) BOLT_PROF_ADD(1, BOLT_CLOCK() - tw0);  // epilogue waits on tfull
             tc_fence_after();
             // copy this warp's 128 columns out of TMEM (packed u16 pairs) and
             // release the accumulator at once, so that a slow filter pass on
@@ -423,12 +496,13 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                 tmem_ld16p(tmem + tlane + (uint32_t)(d * C::N + half * kCols + c * 32), p[c]);
             tmem_wait_ld();
             }
-            if (threadIdx.x == 128) BOLT_PROF_ADD(2, BOLT_CLOCK() - tw0);  // wait + TMEM load
+            if (threadIdx.x == 0) BOLT_PROF_ADD(2, BOLT_CLOCK() - tw0);  // wait + TMEM load
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
+                BOLT_TRACE(tile, 19 + warp);
                 if (rank == 0) mbar_arrive(&tempty[d]);
-                else mbar_arrive_cluster(&tempty[d], 0);
+                else mbar_arrive_cluster_relaxed(&tempty[d], 0);
             }
             const long long tp0 = BOLT_CLOCK();
             if (xmode & 1) continue;  // diagnostic: load + release only
@@ -498,6 +572,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             }
             __syncwarp();  // reconverge before the next tile's .aligned tcgen05.ld
             if (lane == 0) BOLT_PROF_ADD(8, BOLT_CLOCK() - tp0);  // processing cycles (all warps)
+            if (lane == 0) BOLT_TRACE(tile, 27 + warp);
             if (own < published && qvalid) {
                 published = own;
                 asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gq), "r"(0xFFFFu - own) : "memory");
@@ -532,7 +607,9 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                 mbar_wait_cluster(&tempty[d], ((tile >> 1) & 1) ^ 1);
                 long long t2 = BOLT_CLOCK();
                 BOLT_PROF_ADD(3, t1 - t0);  // MMA waits on full
+                BOLT_TRACE(tile, 0);
                 BOLT_PROF_ADD(4, t2 - t1);  // MMA waits on tempty
+                BOLT_TRACE(tile, 1);
                 BOLT_PROF_ADD(5, 1);        // tiles
                 tc_fence_after();
                 const uint32_t bs = b_base + s * C::B_BYTES;
@@ -545,6 +622,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                 }
                 mma_commit_pair(&empty[s]);
                 mma_commit_pair(&tfull[d]);
+                BOLT_TRACE(tile, 2);
             }
         }
         __syncwarp();

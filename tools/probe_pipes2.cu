@@ -19,6 +19,10 @@ __device__ __forceinline__ uint32_t op(uint32_t a, uint32_t b) {
     if (OP == 7) asm volatile("add.rn.f32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
     if (OP == 8) asm volatile("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
     if (OP == 9) asm volatile("prmt.b32 %0, %1, %2, 0x3210;" : "=r"(d) : "r"(a), "r"(b));
+    if (OP == 10) asm volatile("add.u32 %0, %1, 1234;" : "=r"(d) : "r"(a));
+    if (OP == 11) asm volatile("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    if (OP == 12) asm volatile("mad.lo.u32 %0, %1, 8, -96;" : "=r"(d) : "r"(a));
+    if (OP == 13) asm volatile("shl.b32 %0, %1, 3;" : "=r"(d) : "r"(a));
     return d;
 }
 __device__ __forceinline__ uint32_t lop(uint32_t a, uint32_t b) {
@@ -81,5 +85,9 @@ int main() {
     run<6>("shl.b32", out, cyc);
     run<7>("add.f32", out, cyc);
     run<9>("prmt", out, cyc);
+    run<10>("add.u32 imm", out, cyc);
+    run<11>("add.f16x2", out, cyc);
+    run<12>("mad imm 8,-96", out, cyc);
+    run<13>("shl imm", out, cyc);
     return 0;
 }

@@ -1,1 +1,2 @@
-for x in 0 16; do echo "xmode=$x"; BOLT_LIB=libbolt_x.so BOLT_TC_XMODE=$x timeout 120 python tools/prof_scan.py --variant tc --reps 5 --config c2 $([ $x = 16 ] && echo --prefill); done
+bash tools/ab.sh libbolt_base.so libbolt.so
+for x in 64 65; do echo "== xmode=$x"; BOLT_LIB=libbolt_x.so BOLT_TC_XMODE=$x TRACE_OUT=gpurun_out/trace_$x.npy timeout 120 python tools/trace_scan.py --variant tc --config c2; done
