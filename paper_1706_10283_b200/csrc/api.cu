@@ -115,15 +115,16 @@ TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     p.variant = v;
     p.parts = v == BOLT_VARIANT_TC ? topk_tc_parts(n, m, nq, k, sms) : topk_prmt_parts(n, m, nq, k, sms);
     p.ws = p.parts > 1 ? (size_t)p.parts * nq * k * sizeof(uint64_t) : 0;
-    // both variants keep a per-query shared threshold array (u32) after the partial lists
-    if (p.ws > 0) p.ws += (size_t)nq * sizeof(uint32_t);
+    // shared per-query thresholds (u32) after the partial lists: PRMT one word,
+    // TC 3 nq + 1 (k-th value words + 8 B aligned half-list pairs, scan_tc.cu)
+    if (p.ws > 0) p.ws += (size_t)(v == BOLT_VARIANT_TC ? 3 * nq + 1 : nq) * sizeof(uint32_t);
     if (v == BOLT_VARIANT_TC && p.parts > 1) {
         p.pre_n = tc_prefix_rows(n);
         if (p.pre_n > 0) {
             p.pre_parts = topk_tc_parts(p.pre_n, m, nq, k, sms);
             if (p.pre_parts > 32) p.pre_parts = 32;
             p.pre_off = align256(p.ws);
-            p.ws = p.pre_off + (size_t)p.pre_parts * nq * k * sizeof(uint64_t) + (size_t)nq * sizeof(uint32_t);
+            p.ws = p.pre_off + (size_t)p.pre_parts * nq * k * sizeof(uint64_t) + (size_t)(3 * nq + 1) * sizeof(uint32_t);
         }
     }
     return p;

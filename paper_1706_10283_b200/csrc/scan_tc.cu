@@ -468,11 +468,23 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
         // value can reach the global top-k only if kv' < own and kv' <= T.
         uint32_t own = kNotFull;
         uint32_t published = kNotFull;
+        // Half-list bound: the ceil(k/2)-th value of this list.  The lists of
+        // the two column halves cover disjoint vectors, so if the best half-0
+        // list and the best half-1 list each hold ceil(k/2) values <= x, the
+        // union holds >= k of them: T2 = max over the two halves of the
+        // per-half minimum of that value is also a valid threshold.  Kept in
+        // two more inverted words per query (gthr_inv[hoff + 2q + half], hoff =
+        // nq rounded up to even).
+        const int hpos = KMAX - 1 - k / 2;
+        uint32_t published_h = k > 1 ? kNotFull : 0u;
+        bool changed = false;  // list changed since the half bound was last published
         const bool qvalid = q0 + q < a.nq;
         uint32_t* gq = gthr_inv + (qvalid ? q0 + q : 0);
         uint32_t thr = kNotFull;
-        uint32_t g_next;  // inverted shared threshold (0 = none yet), fetched a tile ahead
+        uint32_t* gh = gthr_inv + ((a.nq + 1) & ~int64_t(1)) + 2 * (qvalid ? q0 + q : 0);  // 8 B aligned
+        uint32_t g_next, gh0, gh1;  // inverted shared thresholds (0 = none yet), fetched a tile ahead
         asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g_next) : "l"(gq));
+        asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gh0), "=r"(gh1) : "l"(gh));
         const uint32_t tlane = (uint32_t)(quad * 32) << 16;
         for (int tile = 0; tile < ntiles; ++tile) {
             const int d = tile & 1;
@@ -507,10 +519,11 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             const long long tp0 = BOLT_CLOCK();
             if (xmode & 1) continue;  // diagnostic: load + release only
             // shared threshold: use the value fetched one tile ago, prefetch the next
-            thr = min(own, 0xFFFFu - g_next + 1u);
+            thr = min(min(own, 0xFFFFu - g_next + 1u), 0xFFFFu - min(gh0, gh1) + 1u);
             if (tile >= 1 && thr > 0xFFFFu) BOLT_PROF_WARP(17, 1);  // lanes without a threshold after tile 0
             if (tile == 1) BOLT_PROF_ADD(18, thr);
             asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g_next) : "l"(gq));
+            asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gh0), "=r"(gh1) : "l"(gh));
             const int tbl = tile * C::N;  // local index of the tile's first vector
             const int nvalid = (int)min64(C::N, vend - vbeg - tbl);
             // packed u16x2 tree over the warp's 128 columns; the four chunk
@@ -534,6 +547,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             const bool tail = nvalid < C::N;
             if (xmode & 4) {  // diagnostic: filter only, never the slow path
                 if (kvbest == 0xFFFFFFFFu) list.insert(kvbest);
+                if (lane == 0) BOLT_TRACE(tile, 27 + warp);
                 continue;
             }
             if (kvbest < thr || tail) {
@@ -565,6 +579,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                             list.insert((kv << C::IDX_BITS) | (uint32_t)(tbl + col + j));
                             own = list.threshold(C::IDX_BITS);
                             thr = min(thr, own);
+                            changed = true;
                             BOLT_PROF_WARP(10, 1);  // inserts
                         }
                     }
@@ -576,6 +591,15 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             if (own < published && qvalid) {
                 published = own;
                 asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gq), "r"(0xFFFFu - own) : "memory");
+            }
+            if (changed && qvalid) {
+                changed = false;
+                const uint32_t own_h = list.value_at(hpos, C::IDX_BITS);
+                if (own_h < published_h) {  // published_h = 0 for k == 1 (the half bound is own)
+                    published_h = own_h;
+                    asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gh + half), "r"(0xFFFFu - own_h)
+                                 : "memory");
+                }
             }
         }
         if (q0 + q < a.nq) {
@@ -662,8 +686,11 @@ cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, 
 #ifdef BOLT_XMODE
     if (const char* x = getenv("BOLT_TC_XMODE")) xmode = atoi(x);
 #endif
-    if (init_thr && !(xmode & 16)) {  // diagnostic 16: keep caller-prefilled shared thresholds
-        cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)a.nq * sizeof(uint32_t), s);
+    // shared thresholds: [nq] k-th-value words, then (8 B aligned) [nq][2] half-list words
+    if (!(xmode & 16)) {  // diagnostic 16: keep caller-prefilled shared thresholds
+        const int64_t hoff = (a.nq + 1) & ~int64_t(1);
+        cudaError_t e = init_thr ? cudaMemsetAsync(gthr, 0, (size_t)(hoff + 2 * a.nq) * sizeof(uint32_t), s)
+                                 : cudaMemsetAsync(gthr + hoff, 0, (size_t)a.nq * 2 * sizeof(uint32_t), s);
         if (e != cudaSuccess) return e;
     }
     return cudaLaunchKernelEx(&cfg, kern, a, k, index_base, vpp, tiles_q, part_keys, gthr, xmode);
