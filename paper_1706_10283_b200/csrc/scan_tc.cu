@@ -272,13 +272,17 @@ struct RegList {
 #pragma unroll
         for (int i = 0; i < KMAX; ++i) v[i] = i < KMAX - k ? 0u : 0xFFFFFFFFu;
     }
+    // Insert c, evicting the largest key.  All comparisons against the old
+    // list are independent, then each slot selects its old value, c, or its
+    // left neighbour (depth 3, instead of a KMAX-long min/max chain: the
+    // slow path is latency-bound).
     __device__ __forceinline__ void insert(uint32_t c) {
+        bool lt[KMAX];
 #pragma unroll
-        for (int i = 0; i < KMAX; ++i) {
-            const uint32_t lo = min(v[i], c);
-            c = max(v[i], c);
-            v[i] = lo;
-        }
+        for (int i = 0; i < KMAX; ++i) lt[i] = v[i] < c;
+#pragma unroll
+        for (int i = KMAX - 1; i > 0; --i) v[i] = lt[i] ? v[i] : (lt[i - 1] ? c : v[i - 1]);
+        v[0] = lt[0] ? v[0] : c;
     }
     __device__ __forceinline__ uint32_t threshold(int idx_bits) const {
         return v[KMAX - 1] == 0xFFFFFFFFu ? kNotFull : (v[KMAX - 1] >> idx_bits);
