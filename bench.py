@@ -146,7 +146,7 @@ def workload(args, rank):
     return cfg, n, nq
 
 
-def cpu_baseline_sample(cfg, X, Q, C, a, b, metric, k, budget_s=20.0):
+def cpu_baseline_sample(cfg, X, Q, C, a, b, metric, k, budget_s=20.0, dequant=False):
     """The fp64 oracle, as it stands, on the host cores: encode of the full
     database shard, tables of all queries, and the scan + top-k for a sample
     of queries over the full database; the scan time is scaled to all
@@ -161,17 +161,26 @@ def cpu_baseline_sample(cfg, X, Q, C, a, b, metric, k, budget_s=20.0):
     ql = oracle.quantize(oracle.luts(Q, C, metric), a, b)
     t_lut = time.perf_counter() - t0
     # size the scan sample to the remaining budget (at least 8 queries)
+    def scan_part(qn):
+        if k > 0:
+            oracle.topk(flat, ql[:qn], k, metric)
+        else:
+            acc = oracle.scan(flat, ql[:qn])
+            if dequant:
+                oracle.dequant(acc, a, b)
+
     t0 = time.perf_counter()
-    oracle.topk(flat, ql[:8], k, metric)
+    scan_part(8)
     t8 = time.perf_counter() - t0
     qs = int(max(8, min(nq, 8 * max(1.0, (budget_s - t_enc - t_lut - t8) / max(t8, 1e-3)))))
     qs = min(qs, 1024)
     t0 = time.perf_counter()
-    oracle.topk(flat, ql[:qs], k, metric)
+    scan_part(qs)
     t_scan = time.perf_counter() - t0
     t_full = t_enc + t_lut + t_scan * (nq / qs)
     desc = (f"oracle encode of all {n} rows ({t_enc:.2f} s) + fp64 tables of all {nq} queries "
-            f"({t_lut:.2f} s) + scan/top-{k} of {qs} queries over all rows ({t_scan:.2f} s), "
+            f"({t_lut:.2f} s) + scan{f'/top-{k}' if k else (' + dequant' if dequant else '')} of {qs} queries "
+            f"over all rows ({t_scan:.2f} s), "
             f"scan scaled x{nq / qs:.1f} to {nq} queries")
     return n * nq / t_full / 1e9, threads, desc
 
@@ -213,18 +222,31 @@ def run_ours(args):
     words = bolt.codes_words(n, cfg.m)
     codes = torch.empty(words, dtype=torch.uint32, device=dev)
     ql = torch.empty((nq, cfg.m, 16), dtype=torch.uint8, device=dev)
-    keys = torch.empty((nq, k), dtype=torch.uint64, device=dev)
-    wsb = bolt.topk_workspace_bytes(n, cfg.m, nq, k, variant)
-    ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
-    gathered = torch.empty((world, nq, k), dtype=torch.uint64, device=dev) if world > 1 else None
-    final = torch.empty((nq, k), dtype=torch.uint64, device=dev) if world > 1 else keys
+    full = k == 0  # c1 / c4: full [N][Q] output (u16 sums, or dequantised fp32 for c4), no top-k
     ev_scan = []
+    if full:
+        b_sum = float(model.b.sum().item())
+        out = torch.empty((n, nq), dtype=torch.float32 if cfg.cid == 4 else torch.uint16, device=dev)
+
+        def scan_op():
+            if cfg.cid == 4:
+                bolt.scan_dequant(codes, n, ql, model.a, b_sum, out=out, variant=variant)
+            else:
+                bolt.scan(codes, n, ql, out=out, variant=variant)
+    else:
+        keys = torch.empty((nq, k), dtype=torch.uint64, device=dev)
+        wsb = bolt.topk_workspace_bytes(n, cfg.m, nq, k, variant)
+        ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
+        final = torch.empty((nq, k), dtype=torch.uint64, device=dev) if world > 1 else keys
+
+        def scan_op():
+            bolt.topk(codes, n, ql, k, metric, index_base=rank * n, variant=variant, out=keys, workspace=ws)
 
     def step():
         bolt.encode(Xd, model.C, out=codes)
         bolt.build_quantized_luts(Qd, model.C, metric, model.a, model.b, out=ql)
-        bolt.topk(codes, n, ql, k, metric, index_base=rank * n, variant=variant, out=keys, workspace=ws)
-        if world > 1:
+        scan_op()
+        if world > 1 and not full:
             bolt.topk_merge(gather_keys(keys), out=final)
 
     for _ in range(args.warmup):
@@ -270,7 +292,7 @@ def run_ours(args):
         for _ in range(args.steps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            bolt.topk(codes, n, ql, k, metric, index_base=rank * n, variant=variant, out=keys, workspace=ws)
+            scan_op()
             e1.record(stream)
             ev_scan.append((e0, e1))
         torch.cuda.synchronize()
@@ -289,7 +311,34 @@ def run_ours(args):
 
     # --- e2e through the public host-buffer API (H2D of X, Q inside the timed region)
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and full:
+        # full output through the public API: pinned host X, Q in, the [N][Q] result out
+        Xh = torch.from_numpy(X).pin_memory()
+        Qh = torch.from_numpy(Q).pin_memory()
+        outh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        Xd2, Qd2 = torch.empty_like(Xd), torch.empty_like(Qd)
+
+        def e2e_full():
+            Xd2.copy_(Xh, non_blocking=True)
+            Qd2.copy_(Qh, non_blocking=True)
+            bolt.encode(Xd2, model.C, out=codes)
+            bolt.build_quantized_luts(Qd2, model.C, metric, model.a, model.b, out=ql)
+            scan_op()
+            outh.copy_(out, non_blocking=True)
+
+        e2e_full()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_full()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a0.elapsed_time(a1) / args.e2e_steps
+        e2e = {"value": round(n * nq / (e_ms * 1e-3) / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": int(X.nbytes + Q.nbytes), "d2h_bytes_per_step": int(out.numel() * out.element_size()),
+               "ms_per_step": round(e_ms, 3), "api": "bolt.encode / build_quantized_luts / scan* (pinned host buffers)"}
+    elif args.e2e_steps > 0:
         hs = bolt.HostSearch(n, cfg.j, cfg.m, nq, k, device=dev)
         Xh = torch.from_numpy(X).pin_memory()
         Qh = torch.from_numpy(Q).pin_memory()
@@ -323,10 +372,19 @@ def run_ours(args):
                "d2h_bytes_per_step": int(nq * k * 8), "ms_per_step": round(e_ms, 3),
                "api": "bolt_search_host (pinned host X, Q -> keys)"}
 
-    # --- roofline of the dominant kernel (scan + fused top-k)
+    # --- roofline of the dominant kernel (scan + fused top-k, or the full-output scan)
     peaks, peak_src = measured_peaks()
-    used_variant, parts = bolt.topk_plan(n, cfg.m, nq, k, variant)
-    roof = roofline(used_variant, n, cfg.m, nq, scan_ms, peaks, peak_src, clk.summary())
+    if full:
+        used_variant = "tc" if variant == bolt.VARIANT_TC or (variant == bolt.VARIANT_AUTO and nq >= 64 and
+                                                              cfg.m in (8, 16, 32)) else "prmt"
+        parts = 1
+        roof = roofline_full(used_variant, n, cfg.m, nq, out.element_size(), scan_ms, peaks, peak_src)
+    else:
+        used_variant, parts = bolt.topk_plan(n, cfg.m, nq, k, variant)
+        roof = roofline(used_variant, n, cfg.m, nq, scan_ms, peaks, peak_src, clk.summary())
+    mname = "dot product" if metric == bolt.DOT else "squared L2"
+    what = (f"full [N][Q] {'fp32 dequantised (acc/a + sum b)' if cfg.cid == 4 else 'u16'} output" if full
+            else f"top-{k}")
 
     if rank == 0:
         out = {
@@ -335,26 +393,42 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded SIFT1M-like Gaussian mixture, SURVEY 8(d) c2 recipe)",
             "config": {"workload": f"{args.config}: N={n} rows/GPU x J={cfg.j} fp32, M={cfg.m} (4-bit codes), "
-                                   f"Q={nq}, squared L2, top-{k}; step = encode + fp64 LUT build/quantize "
-                                   f"+ scan/top-k" + (" + NCCL all-gather + merge" if world > 1 else ""),
+                                   f"Q={nq}, {mname}, {what}; step = encode + fp64 LUT build/quantize "
+                                   f"+ scan" + ("" if full else "/top-k") +
+                                   (" + NCCL all-gather + merge" if world > 1 and not full else ""),
                        "n_per_gpu": n, "nq": nq, "m": cfg.m, "j": cfg.j, "k": k,
                        "variant": used_variant, "scan_parts": parts, "timing": graph_note,
                        "l2": "inputs > L2: the 512 MB fp32 database is streamed by the encoder every step",
                        "parallelism": f"row-sharded dp{world}"},
             "roofline": roof,
             "e2e": e2e,
-            "gpu_launches": args.steps * (3 + (1 if parts > 1 else 0) + (1 if world > 1 else 0)),
+            "gpu_launches": args.steps * (3 + (1 if parts > 1 else 0) + (1 if world > 1 and not full else 0)),
             "clocks": clk.summary(),
             "scan_ms": round(scan_ms, 4),
         }
         if not args.no_cpu_baseline and world == 1:
             v, cores, desc = cpu_baseline_sample(cfg, X, Q, model.C.cpu().numpy(), np.float32(model.a),
-                                                 model.b.cpu().numpy(), metric, k)
+                                                 model.b.cpu().numpy(), metric, k, dequant=cfg.cid == 4)
             out["cpu_baseline"] = {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
                                    "sample": desc}
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
+
+
+def roofline_full(variant, n, m, nq, out_bytes, scan_ms, peaks, peak_src):
+    """Full-output scan (c1 u16, c4 fp32): bound by the HBM write of the
+    [N][Q] output.  Algorithmic bytes = codes (N*M/2) + u8 tables (Q*16*M) +
+    output (N*Q*out_bytes); peak = measured copy bandwidth (MEASURED_PEAKS.json)."""
+    t = scan_ms * 1e-3
+    algo = n * m // 2 + nq * 16 * m + n * nq * out_bytes
+    gbs = algo / t / 1e9
+    peak = peaks["hbm_gbs"]
+    return {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 4),
+            "traffic": None, "algorithmic_bytes": algo,
+            "peak_source": f"{peak_src} HBM copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+            "kernel": f"bolt_scan{'_dequant' if out_bytes == 4 else ''} ({variant})", "kernel_ms": round(scan_ms, 4),
+            "tensor_view": {"int8_tops": round(2.0 * 16 * m * n * nq / t / 1e12, 1)} if variant == "tc" else None}
 
 
 def roofline(variant, n, m, nq, scan_ms, peaks, peak_src, clocks):

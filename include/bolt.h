@@ -138,6 +138,17 @@ BOLT_API bolt_status bolt_scan_dequant(const uint32_t* codes, int64_t n, int m, 
                               int64_t nq, float a, float b_sum, float* out, int64_t ldo,
                               bolt_stream_t stream);
 
+/* As bolt_scan / bolt_scan_dequant with an explicit implementation:
+ * BOLT_VARIANT_AUTO (tcgen05 when nq >= 64 and m is 8, 16 or 32, else
+ * PRMT), BOLT_VARIANT_PRMT, or BOLT_VARIANT_TC (BOLT_E_RANGE for other m).
+ * Both variants return the same integers bit for bit; the fp32 output is
+ * fmaf((float)acc, 1/a, b_sum) in both. */
+BOLT_API bolt_status bolt_scan_ex(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts, int64_t nq,
+                                  uint16_t* out, int64_t ldo, int variant, bolt_stream_t stream);
+BOLT_API bolt_status bolt_scan_dequant_ex(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts,
+                                          int64_t nq, float a, float b_sum, float* out, int64_t ldo, int variant,
+                                          bolt_stream_t stream);
+
 /* --------------------------------------------------------------- top-k */
 /* k best database vectors per query ("the k closest"; NN and MIPS,
  * P:L33) by the 64-bit key (R13)

@@ -127,28 +127,29 @@ def build_quantized_luts(Q: torch.Tensor, C: torch.Tensor, metric, a: float, b: 
 
 
 # ------------------------------------------------------------------- d^ (scan)
-def scan(codes: torch.Tensor, n: int, qluts: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+def scan(codes: torch.Tensor, n: int, qluts: torch.Tensor, out: torch.Tensor | None = None,
+         variant: int = VARIANT_AUTO) -> torch.Tensor:
     """Exact u16 sums [n][nq] (row = database vector)."""
     _cuda(codes, "codes", torch.uint32)
     _cuda(qluts, "qluts", torch.uint8)
     nq, m, _ = qluts.shape
     if out is None:
         out = torch.empty((n, nq), dtype=torch.uint16, device=codes.device)
-    _lib.call("bolt_scan", codes.data_ptr(), n, m, qluts.data_ptr(), nq, out.data_ptr(), out.stride(0),
-              _stream(codes.device))
+    _lib.call("bolt_scan_ex", codes.data_ptr(), n, m, qluts.data_ptr(), nq, out.data_ptr(), out.stride(0),
+              int(variant), _stream(codes.device))
     return out
 
 
 def scan_dequant(codes: torch.Tensor, n: int, qluts: torch.Tensor, a: float, b_sum: float,
-                 out: torch.Tensor | None = None) -> torch.Tensor:
+                 out: torch.Tensor | None = None, variant: int = VARIANT_AUTO) -> torch.Tensor:
     """fp32 [n][nq] = acc / a + sum_m b_m (approximate A.B)."""
     _cuda(codes, "codes", torch.uint32)
     _cuda(qluts, "qluts", torch.uint8)
     nq, m, _ = qluts.shape
     if out is None:
         out = torch.empty((n, nq), dtype=torch.float32, device=codes.device)
-    _lib.call("bolt_scan_dequant", codes.data_ptr(), n, m, qluts.data_ptr(), nq, float(a), float(b_sum),
-              out.data_ptr(), out.stride(0), _stream(codes.device))
+    _lib.call("bolt_scan_dequant_ex", codes.data_ptr(), n, m, qluts.data_ptr(), nq, float(a), float(b_sum),
+              out.data_ptr(), out.stride(0), int(variant), _stream(codes.device))
     return out
 
 

@@ -32,6 +32,8 @@ SIGNATURES = {
     "bolt_build_quantized_luts": ([_P, _I64, _I32, _I64, _P, _I32, _I32, _F32, _P, _P, _P, _P], _I32),
     "bolt_scan": ([_P, _I64, _I32, _P, _I64, _P, _I64, _P], _I32),
     "bolt_scan_dequant": ([_P, _I64, _I32, _P, _I64, _F32, _F32, _P, _I64, _P], _I32),
+    "bolt_scan_ex": ([_P, _I64, _I32, _P, _I64, _P, _I64, _I32, _P], _I32),
+    "bolt_scan_dequant_ex": ([_P, _I64, _I32, _P, _I64, _F32, _F32, _P, _I64, _I32, _P], _I32),
     "bolt_topk_workspace_bytes": ([_I64, _I32, _I64, _I32], _SZ),
     "bolt_topk": ([_P, _I64, _I32, _P, _I64, _I32, _I32, _I64, _P, _P, _SZ, _P], _I32),
     "bolt_topk_plan": ([_I64, _I32, _I64, _I32, _I32, _P, _P], _I32),

@@ -253,31 +253,62 @@ static bolt_status scan_common(const uint32_t* codes, int64_t n, int m, const ui
     return BOLT_OK;
 }
 
-bolt_status bolt_scan(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts, int64_t nq,
-                      uint16_t* out, int64_t ldo, bolt_stream_t stream) {
+// Full-output scan dispatch: the tcgen05 contraction for batched queries
+// (nq >= 64, m in {8, 16, 32}), else the PRMT kernel.
+static int scan_variant(int64_t n, int m, int64_t nq, int variant) {
+    if (variant == BOLT_VARIANT_AUTO) return scan_tc_supported(n, m, nq) && nq >= 64 ? BOLT_VARIANT_TC : BOLT_VARIANT_PRMT;
+    return variant;
+}
+
+bolt_status bolt_scan_ex(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts, int64_t nq,
+                         uint16_t* out, int64_t ldo, int variant, bolt_stream_t stream) {
     TRY(scan_common(codes, n, m, qluts, nq));
     if (ldo < nq) return fail(BOLT_E_SHAPE, "ldo = %lld < nq = %lld", (long long)ldo, (long long)nq);
+    if (variant < BOLT_VARIANT_AUTO || variant > BOLT_VARIANT_TC) return fail(BOLT_E_RANGE, "variant %d", variant);
+    if (variant == BOLT_VARIANT_TC && !scan_tc_supported(n, m, nq))
+        return fail(BOLT_E_RANGE, "tcgen05 scan does not support m=%d", m);
     if (n == 0 || nq == 0) return BOLT_OK;
     if (!out) return fail(BOLT_E_NULL, "out NULL");
     DevInfo d;
     TRY(device_info(&d));
     ScanArgs a{codes, n, ceil_div(n, 8), m, qluts, nq};
-    return cuda_status(launch_scan_full(a, out, nullptr, ldo, 0.f, 0.f, (cudaStream_t)stream), "bolt_scan");
+    cudaStream_t s = (cudaStream_t)stream;
+    return cuda_status(scan_variant(n, m, nq, variant) == BOLT_VARIANT_TC
+                           ? launch_scan_tc(a, out, nullptr, ldo, 0.f, 0.f, d.sms, s)
+                           : launch_scan_full(a, out, nullptr, ldo, 0.f, 0.f, s),
+                       "bolt_scan");
 }
 
-bolt_status bolt_scan_dequant(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts,
-                              int64_t nq, float a, float b_sum, float* out, int64_t ldo,
-                              bolt_stream_t stream) {
+bolt_status bolt_scan(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts, int64_t nq,
+                      uint16_t* out, int64_t ldo, bolt_stream_t stream) {
+    return bolt_scan_ex(codes, n, m, qluts, nq, out, ldo, BOLT_VARIANT_AUTO, stream);
+}
+
+bolt_status bolt_scan_dequant_ex(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts,
+                                 int64_t nq, float a, float b_sum, float* out, int64_t ldo, int variant,
+                                 bolt_stream_t stream) {
     TRY(scan_common(codes, n, m, qluts, nq));
     if (ldo < nq) return fail(BOLT_E_SHAPE, "ldo = %lld < nq = %lld", (long long)ldo, (long long)nq);
     if (!(a > 0.f)) return fail(BOLT_E_RANGE, "a = %g must be > 0", (double)a);
+    if (variant < BOLT_VARIANT_AUTO || variant > BOLT_VARIANT_TC) return fail(BOLT_E_RANGE, "variant %d", variant);
+    if (variant == BOLT_VARIANT_TC && !scan_tc_supported(n, m, nq))
+        return fail(BOLT_E_RANGE, "tcgen05 scan does not support m=%d", m);
     if (n == 0 || nq == 0) return BOLT_OK;
     if (!out) return fail(BOLT_E_NULL, "out NULL");
     DevInfo d;
     TRY(device_info(&d));
     ScanArgs sa{codes, n, ceil_div(n, 8), m, qluts, nq};
-    return cuda_status(launch_scan_full(sa, nullptr, out, ldo, 1.0f / a, b_sum, (cudaStream_t)stream),
+    cudaStream_t s = (cudaStream_t)stream;
+    return cuda_status(scan_variant(n, m, nq, variant) == BOLT_VARIANT_TC
+                           ? launch_scan_tc(sa, nullptr, out, ldo, 1.0f / a, b_sum, d.sms, s)
+                           : launch_scan_full(sa, nullptr, out, ldo, 1.0f / a, b_sum, s),
                        "bolt_scan_dequant");
+}
+
+bolt_status bolt_scan_dequant(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts,
+                              int64_t nq, float a, float b_sum, float* out, int64_t ldo,
+                              bolt_stream_t stream) {
+    return bolt_scan_dequant_ex(codes, n, m, qluts, nq, a, b_sum, out, ldo, BOLT_VARIANT_AUTO, stream);
 }
 
 size_t bolt_topk_workspace_bytes_ex(int64_t n, int m, int64_t nq, int k, int variant) {

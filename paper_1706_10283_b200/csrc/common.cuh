@@ -114,6 +114,9 @@ cudaError_t launch_topk_prmt(const ScanArgs& a, int k, int metric, int64_t index
                              uint64_t* part_keys, int sms, cudaStream_t s);
 // top-k (tcgen05 variant)
 int topk_tc_supported(int64_t n, int m, int64_t nq, int k);
+int scan_tc_supported(int64_t n, int m, int64_t nq);
+cudaError_t launch_scan_tc(const ScanArgs& a, uint16_t* out16, float* out32, int64_t ldo, float inv_a, float b_sum,
+                           int sms, cudaStream_t s);
 int topk_tc_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
 // part_keys: parts*nq*k keys followed by nq u32 shared thresholds (zeroed
 // by the launch when init_thresholds, else seeded by the caller)

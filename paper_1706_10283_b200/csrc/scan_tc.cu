@@ -319,10 +319,19 @@ __device__ __forceinline__ uint32_t candidate_mask(const uint32_t (&p)[16], uint
     return ~nm;
 }
 
-template <int M, bool kDot, int KMAX>
+// Full-output mode (kOut = 1: u16 sums, 2: fp32 acc / a + sum b):
+// out[i * ldo + q] for database vector i and query q.
+struct FullOut {
+    void* out;
+    int64_t ldo;
+    float inv_a, b_sum;
+    int vec;  // rows 16 B aligned: vector stores
+};
+
+template <int M, bool kDot, int KMAX, int kOut = 0>
 __global__ void __launch_bounds__(kThreads, 1)
 topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, uint64_t* __restrict__ part_keys,
-               uint32_t* __restrict__ gthr_inv, int xmode) {
+               uint32_t* __restrict__ gthr_inv, int xmode, FullOut fo) {
 #ifndef BOLT_XMODE
     xmode = 0;  // diagnostic stage switches exist only in libbolt_x.so (tools/)
 #endif
@@ -522,6 +531,53 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             }
             const long long tp0 = BOLT_CLOCK();
             if (xmode & 1) continue;  // diagnostic: load + release only
+            if constexpr (kOut != 0) {
+                // full output, swapped roles: this thread = database vector (TMEM
+                // lane), registers = 128 consecutive queries of its output row
+                const int64_t vi = vbeg + (int64_t)tile * C::N + rank * C::NH + quad * 32 + lane;
+                const int64_t qb = (int64_t)tq * 2 * kQM + half * kCols;  // first query of this warp
+                if (vi < vend) {
+                    if (kOut == 1) {
+                        uint16_t* row = static_cast<uint16_t*>(fo.out) + vi * fo.ldo + qb;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+#pragma unroll
+                            for (int i = 0; i < 16; i += 4) {
+                                const int64_t qq = qb + c * 32 + 2 * i;  // 8 queries: qq .. qq+7
+                                if (fo.vec && qq + 8 <= a.nq)
+                                    *reinterpret_cast<uint4*>(row + c * 32 + 2 * i) =
+                                        make_uint4(p[c][i], p[c][i + 1], p[c][i + 2], p[c][i + 3]);
+                                else
+#pragma unroll
+                                    for (int e = 0; e < 8; ++e)
+                                        if (qq + e < a.nq)
+                                            row[c * 32 + 2 * i + e] = (uint16_t)(p[c][i + e / 2] >> (16 * (e & 1)));
+                            }
+                    } else {
+                        float* row = static_cast<float*>(fo.out) + vi * fo.ldo + qb;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+#pragma unroll
+                            for (int i = 0; i < 16; i += 2) {
+                                // exact u16 -> fp32: bits 0x4B00xxxx = 2^23 + x, minus 2^23
+                                float f[4];
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    const uint32_t bits = __byte_perm(p[c][i + e / 2], 0x4B000000u, (e & 1) ? 0x7632 : 0x7610);
+                                    f[e] = fmaf(__uint_as_float(bits) - 8388608.0f, fo.inv_a, fo.b_sum);
+                                }
+                                const int64_t qq = qb + c * 32 + 2 * i;  // 4 queries: qq .. qq+3
+                                if (fo.vec && qq + 4 <= a.nq)
+                                    *reinterpret_cast<float4*>(row + c * 32 + 2 * i) = make_float4(f[0], f[1], f[2], f[3]);
+                                else
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e)
+                                        if (qq + e < a.nq) row[c * 32 + 2 * i + e] = f[e];
+                            }
+                    }
+                }
+                continue;
+            }
             // shared threshold: use the value fetched one tile ago, prefetch the next
             thr = min(min(own, 0xFFFFu - g_next + 1u), 0xFFFFu - min(gh0, gh1) + 1u);
             if (tile >= 1 && thr > 0xFFFFu) BOLT_PROF_WARP(17, 1);  // lanes without a threshold after tile 0
@@ -606,7 +662,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                 }
             }
         }
-        if (q0 + q < a.nq) {
+        if (kOut == 0 && q0 + q < a.nq) {
             uint64_t* dst = part_keys + ((int64_t)(2 * part + half) * a.nq + q0 + q) * k;
 #pragma unroll
             for (int i = 0; i < KMAX; ++i) {
@@ -646,7 +702,11 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                     // K step ks covers 16-byte chunks 2ks, 2ks+1 (same offsets in the peer CTA)
                     const uint64_t ad = smem_desc(a_base + 2 * ks * (kQM * 16), kQM * 16, 128);
                     const uint64_t bd = smem_desc(bs + 2 * ks * (C::NH * 16), C::NH * 16, 128);
-                    mma_i8_pair(tmem + (uint32_t)(d * C::N), ad, bd, C::IDESC, ks > 0 ? 1u : 0u);
+                    // top-k: D[query][vector] (A = tables); full output: the roles swap,
+                    // D[vector][query] (A = one-hot), so that an epilogue thread owns
+                    // consecutive queries of one output row
+                    if (kOut == 0) mma_i8_pair(tmem + (uint32_t)(d * C::N), ad, bd, C::IDESC, ks > 0 ? 1u : 0u);
+                    else mma_i8_pair(tmem + (uint32_t)(d * C::N), bd, ad, C::IDESC, ks > 0 ? 1u : 0u);
                 }
                 mma_commit_pair(&empty[s]);
                 mma_commit_pair(&tfull[d]);
@@ -666,13 +726,13 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
     }
 }
 
-template <int M, bool kDot, int KMAX>
+template <int M, bool kDot, int KMAX, int kOut = 0>
 cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, uint64_t* part_keys,
-                      uint32_t* gthr, cudaStream_t s, bool init_thr) {
+                      uint32_t* gthr, cudaStream_t s, bool init_thr, FullOut fo = FullOut{}) {
     using C = Cfg<M>;
     const int tiles_q = (int)ceil_div(a.nq, 2 * kQM);
     const int64_t vpp = ceil_div(ceil_div(a.n, rparts), 8) * 8;
-    auto kern = topk_tc_kernel<M, kDot, KMAX>;
+    auto kern = topk_tc_kernel<M, kDot, KMAX, kOut>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(2 * tiles_q * rparts));
@@ -691,13 +751,20 @@ cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, 
     if (const char* x = getenv("BOLT_TC_XMODE")) xmode = atoi(x);
 #endif
     // shared thresholds: [nq] k-th-value words, then (8 B aligned) [nq][2] half-list words
-    if (!(xmode & 16)) {  // diagnostic 16: keep caller-prefilled shared thresholds
+    if (kOut == 0 && !(xmode & 16)) {  // diagnostic 16: keep caller-prefilled shared thresholds
         const int64_t hoff = (a.nq + 1) & ~int64_t(1);
         cudaError_t e = init_thr ? cudaMemsetAsync(gthr, 0, (size_t)(hoff + 2 * a.nq) * sizeof(uint32_t), s)
                                  : cudaMemsetAsync(gthr + hoff, 0, (size_t)a.nq * 2 * sizeof(uint32_t), s);
         if (e != cudaSuccess) return e;
     }
-    return cudaLaunchKernelEx(&cfg, kern, a, k, index_base, vpp, tiles_q, part_keys, gthr, xmode);
+    return cudaLaunchKernelEx(&cfg, kern, a, k, index_base, vpp, tiles_q, part_keys, gthr, xmode, fo);
+}
+
+// full [n][nq] output: u16 sums (out32 == nullptr) or fp32 dequantised
+template <int M>
+cudaError_t launch_full_m(const ScanArgs& a, int rparts, FullOut fo, bool f32, cudaStream_t s) {
+    return f32 ? launch_mk<M, false, 4, 2>(a, 1, 0, rparts, nullptr, nullptr, s, false, fo)
+               : launch_mk<M, false, 4, 1>(a, 1, 0, rparts, nullptr, nullptr, s, false, fo);
 }
 
 template <int M>
@@ -719,6 +786,31 @@ cudaError_t launch_m(const ScanArgs& a, int k, int metric, int64_t index_base, i
 }
 
 }  // namespace tc
+
+int scan_tc_supported(int64_t n, int m, int64_t nq) {
+    return n >= 1 && nq >= 1 && (m == 8 || m == 16 || m == 32);
+}
+
+// Full-output scan on the tensor cores (same pipeline as the top-k scan; the
+// epilogue stores every sum).  Row partitions fill the SM pairs as for top-k.
+cudaError_t launch_scan_tc(const ScanArgs& a, uint16_t* out16, float* out32, int64_t ldo, float inv_a, float b_sum,
+                           int sms, cudaStream_t s) {
+    // one wave of long units: the per-unit prologue (barriers, TMEM, the
+    // query tables) would dominate short ones
+    const int64_t tiles_q = ceil_div(a.nq, 2 * tc::kQM);
+    const int64_t pairs = sms / 2;
+    const int rparts = (int)max64(1, min64(pairs / max64(tiles_q, 1), ceil_div(a.groups, 32)));
+    void* out = out32 ? static_cast<void*>(out32) : static_cast<void*>(out16);
+    const int esz = out32 ? 4 : 2;
+    const int vec = (reinterpret_cast<uintptr_t>(out) % 16 == 0) && ((ldo * esz) % 16 == 0);
+    tc::FullOut fo{out, ldo, inv_a, b_sum, vec};
+    switch (a.m) {
+        case 8: return tc::launch_full_m<8>(a, rparts, fo, out32 != nullptr, s);
+        case 16: return tc::launch_full_m<16>(a, rparts, fo, out32 != nullptr, s);
+        case 32: return tc::launch_full_m<32>(a, rparts, fo, out32 != nullptr, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
 
 int topk_tc_supported(int64_t n, int m, int64_t nq, int k) {
     (void)nq;

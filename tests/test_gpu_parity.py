@@ -159,6 +159,53 @@ def test_scan_dequant(bolt, orc):
     assert (np.abs(got - ref) <= tol).all()
 
 
+# tcgen05 full-output scan (one-hot x table contraction, all sums stored):
+# ragged n (several 256-vector tiles + tail), nq across 256-query tiles
+TC_SCAN_SHAPES = [(1, 8, 1), (300, 16, 70), (2049, 32, 257), (5000, 8, 513), (777, 16, 64), (70000, 16, 300)]
+
+
+@pytest.mark.parametrize("n,m,nq", TC_SCAN_SHAPES)
+def test_scan_tc_bitexact(bolt, orc, n, m, nq):
+    flat = G.random_codes(n, m, n + 5 * m)
+    ql = G.random_qluts(nq, m, nq + 7 * m)
+    codes = pack_on_gpu(bolt, flat)
+    got = host(bolt.scan(codes, n, dev(ql), variant=bolt.VARIANT_TC))
+    np.testing.assert_array_equal(got, orc.scan(flat, ql))
+
+
+def test_scan_dequant_tc(bolt, orc):
+    n, m, nq = 3001, 32, 200
+    flat = G.random_codes(n, m, 21)
+    ql = G.random_qluts(nq, m, 22)
+    a, b = _quant_params(m, 23, -2, 1)
+    acc = orc.scan(flat, ql)
+    ref = orc.dequant(acc, a, b)
+    bsum = np.float32(np.sum(b.astype(np.float64)))
+    codes = pack_on_gpu(bolt, flat)
+    got = host(bolt.scan_dequant(codes, n, dev(ql), float(a), bsum, variant=bolt.VARIANT_TC))
+    tol = 2.0 ** -21 * (np.abs(acc / np.float64(a)) + abs(float(bsum)))
+    assert (np.abs(got - ref) <= tol).all()
+    # same fmaf in both variants: bit-identical
+    prmt = host(bolt.scan_dequant(codes, n, dev(ql), float(a), bsum, variant=bolt.VARIANT_PRMT))
+    np.testing.assert_array_equal(got.view(np.uint32), prmt.view(np.uint32))
+
+
+def test_scan_tc_strided_out(bolt, orc):
+    """ldo > nq: only the first nq columns of each output row are written."""
+    import torch
+    n, m, nq, ldo = 1500, 16, 100, 130
+    flat = G.random_codes(n, m, 31)
+    ql = G.random_qluts(nq, m, 32)
+    buf = torch.full((n, ldo), 0xBEEF, dtype=torch.uint16, device="cuda")
+    codes, qd = pack_on_gpu(bolt, flat), dev(ql)
+    # the binding takes a contiguous out; call the C ABI directly for a strided one
+    bolt._lib.call("bolt_scan_ex", codes.data_ptr(), n, m, qd.data_ptr(), nq,
+                   buf.data_ptr(), ldo, bolt.VARIANT_TC, torch.cuda.current_stream().cuda_stream)
+    got = host(buf)
+    np.testing.assert_array_equal(got[:, :nq], orc.scan(flat, ql))
+    assert (got[:, nq:] == 0xBEEF).all()
+
+
 # ---------------------------------------------------------------------- top-k
 TOPK_CASES = [
     # n, m, nq, k, lut_hi (small -> many ties), index_base

@@ -29,6 +29,7 @@ if a.config:
     # the bench's data: seeded config database, GPU-fitted model, encoded codes, fused tables
     cfg = G.CONFIGS[a.config]
     a.m, a.k = cfg.m, cfg.k
+    a.n = min(a.n, cfg.n)
     train = G.training(cfg)
     model = bolt.BoltModel.fit(torch.from_numpy(train).to(dev), cfg.m,
                                torch.from_numpy(G.kmeans_init_all(cfg, len(train))).to(dev),
@@ -45,6 +46,9 @@ v = {"prmt": bolt.VARIANT_PRMT, "tc": bolt.VARIANT_TC, "auto": bolt.VARIANT_AUTO
 if a.what == "encode":
     X = torch.from_numpy(G.database(G.CONFIGS["c2"], a.n)).to(dev)
     C = torch.from_numpy(G.random_floats((a.m, 16, 128 // a.m), 3, 50.0) + 100).to(dev)
+full_out = None
+if a.what in ("full", "dequant"):
+    full_out = torch.empty((a.n, a.nq), dtype=torch.uint16 if a.what == "full" else torch.float32, device=dev)
 ws = None
 prefill = lambda: None  # noqa: E731
 if a.prefill:
@@ -65,7 +69,9 @@ def once():
     if a.what == "topk":
         bolt.topk(codes, a.n, ql, a.k, metric, variant=v, workspace=ws)
     elif a.what == "full":
-        bolt.scan(codes, a.n, ql)
+        bolt.scan(codes, a.n, ql, out=full_out, variant=v)
+    elif a.what == "dequant":
+        bolt.scan_dequant(codes, a.n, ql, 0.5, 1.0, out=full_out, variant=v)
     elif a.what == "encode":
         bolt.encode(X, C)
 
