@@ -88,6 +88,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // ---- top-k plan shared by workspace sizing and execution
 struct TopkPlan {
     int variant;     // resolved PRMT / TC
+    bool small;      // PRMT: the small-batch kernel (scan_small.cu, nq < 64)
     int parts;
     int64_t pre_n;   // TC: rows of the threshold-seeding prefix pass (0 = none)
     int pre_parts;
@@ -113,8 +114,11 @@ TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     int v = variant;
     if (v == BOLT_VARIANT_AUTO) v = topk_tc_supported(n, m, nq, k) && nq >= 64 ? BOLT_VARIANT_TC : BOLT_VARIANT_PRMT;
     p.variant = v;
-    p.parts = v == BOLT_VARIANT_TC ? topk_tc_parts(n, m, nq, k, sms) : topk_prmt_parts(n, m, nq, k, sms);
-    p.ws = p.parts > 1 ? (size_t)p.parts * nq * k * sizeof(uint64_t) : 0;
+    p.small = v == BOLT_VARIANT_PRMT && topk_small_supported(n, m, nq, k);
+    p.parts = v == BOLT_VARIANT_TC ? topk_tc_parts(n, m, nq, k, sms)
+              : p.small           ? topk_small_parts(n, m, nq, k, sms)
+                                  : topk_prmt_parts(n, m, nq, k, sms);
+    p.ws = p.parts > 1 || p.small ? (size_t)p.parts * nq * k * sizeof(uint64_t) : 0;
     // shared per-query thresholds (u32) after the partial lists: PRMT one word,
     // TC 3 nq + 1 (k-th value words + 8 B aligned half-list pairs, scan_tc.cu)
     if (p.ws > 0) p.ws += (size_t)(v == BOLT_VARIANT_TC ? 3 * nq + 1 : nq) * sizeof(uint32_t);
@@ -367,11 +371,21 @@ bolt_status bolt_topk_ex(const uint32_t* codes, int64_t n, int m, const uint8_t*
         e = launch_prefix_threshold(pre_keys, p.pre_parts, nq, k, metric, 255u * (uint32_t)m, gthr, s);
         if (e != cudaSuccess) return cuda_status(e, "bolt_topk prefix threshold");
         e = launch_topk_tc(a, k, metric, index_base, p.parts, parts_out, d.sms, s, false);
+    } else if (p.small) {
+        if (p.parts == 1) {  // the kernel needs its threshold words: keep them in a 1-list workspace
+            e = launch_topk_small(a, k, metric, index_base, 1, static_cast<uint64_t*>(ws), s);
+            if (e != cudaSuccess) return cuda_status(e, "bolt_topk scan");
+            return cuda_status(cudaMemcpyAsync(out_keys, ws, (size_t)nq * k * sizeof(uint64_t),
+                                               cudaMemcpyDeviceToDevice, s), "bolt_topk copy");
+        }
+        e = launch_topk_small(a, k, metric, index_base, p.parts, parts_out, s);
     } else {
         e = p.variant == BOLT_VARIANT_TC ? launch_topk_tc(a, k, metric, index_base, p.parts, parts_out, d.sms, s)
                                          : launch_topk_prmt(a, k, metric, index_base, p.parts, parts_out, d.sms, s);
     }
     if (e != cudaSuccess) return cuda_status(e, "bolt_topk scan");
+    if (p.small && p.parts > 64)
+        return cuda_status(launch_merge_many(parts_out, p.parts, nq, k, out_keys, s), "bolt_topk merge");
     if (p.parts > 1) return cuda_status(launch_merge(parts_out, p.parts, nq, k, out_keys, s), "bolt_topk merge");
     return BOLT_OK;
 }

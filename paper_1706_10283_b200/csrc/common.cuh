@@ -122,6 +122,13 @@ int topk_tc_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
 // by the launch when init_thresholds, else seeded by the caller)
 cudaError_t launch_topk_tc(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
                            uint64_t* part_keys, int sms, cudaStream_t s, bool init_thresholds = true);
+// small query batches (scan_small.cu): one partial list per warp + shared thresholds
+int topk_small_supported(int64_t n, int m, int64_t nq, int k);
+int topk_small_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
+cudaError_t launch_topk_small(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
+                              uint64_t* part_keys, cudaStream_t s);
+// merge of many lists (k <= 32): bound by the k-th smallest head, then select
+cudaError_t launch_merge_many(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out, cudaStream_t s);
 cudaError_t launch_prefix_threshold(const uint64_t* keys, int w, int64_t nq, int k, int metric, uint32_t kvmax,
                                     uint32_t* gthr, cudaStream_t s);
 constexpr int kMaxParts = 16384;  // merge limit (shared memory of the tournament merge)
