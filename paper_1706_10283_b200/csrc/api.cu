@@ -120,8 +120,9 @@ TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
                                   : topk_prmt_parts(n, m, nq, k, sms);
     p.ws = p.parts > 1 || p.small ? (size_t)p.parts * nq * k * sizeof(uint64_t) : 0;
     // shared per-query thresholds (u32) after the partial lists: PRMT one word,
-    // TC 3 nq + 1 (k-th value words + 8 B aligned half-list pairs, scan_tc.cu)
-    if (p.ws > 0) p.ws += (size_t)(v == BOLT_VARIANT_TC ? 3 * nq + 1 : nq) * sizeof(uint32_t);
+    // TC 3 nq + 1 (k-th value words + 8 B aligned half-list pairs, scan_tc.cu),
+    // small-batch PRMT 33 nq (k-th value word + 32 minima slots, scan_small.cu)
+    if (p.ws > 0) p.ws += (size_t)(v == BOLT_VARIANT_TC ? 3 * nq + 1 : p.small ? 33 * nq : nq) * sizeof(uint32_t);
     if (v == BOLT_VARIANT_TC && p.parts > 1) {
         p.pre_n = tc_prefix_rows(n);
         if (p.pre_n > 0) {

@@ -27,6 +27,7 @@ namespace small {
 constexpr int kThreads = 256;  // 8 warps
 constexpr int kWarpsPB = kThreads / 32;
 constexpr int kBlocksPerSM = 2;
+constexpr int kMaxSlots = 32;  // minima slots per query (k <= 32)
 
 template <int QT, int M>
 __device__ __forceinline__ void load_group(const uint32_t* __restrict__ codes, int64_t g, bool valid,
@@ -148,7 +149,13 @@ topk_small_kernel(ScanArgs a, int k, int metric, int64_t index_base, int tiles, 
     uint4* tab = small_smem;  // [QT][M][2], shared by the block
     uint64_t* lists = reinterpret_cast<uint64_t*>(small_smem + QT * M * 2) + warp * QT * k;
     uint32_t* qstate = reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t*>(small_smem + QT * M * 2) +
-                                                   kWarpsPB * QT * k) + warp * 2 * QT;  // [QT] pub, [QT] shr
+                                                   kWarpsPB * QT * k) + warp * 3 * QT;  // [QT] pub, shr, pub min
+    // minima slots: gslot[q][s] = 0xFFFF - min over the warps of slot s of their
+    // best value.  k slots filled by k distinct warps = k distinct rows, so
+    // the largest slot value bounds the k-th best key of the union of all
+    // warps' rows (much tighter than any single warp's k-th).
+    uint32_t* gslot = gthr_inv + a.nq;
+    const int myslot = (int)((blk * kWarpsPB + warp) % k);
     const uint32_t flip = metric == BOLT_DOT ? 0xFFFFFFFFu : 0u;  // kv = 0xFFFF - acc for dot (R13)
     for (int e = threadIdx.x; e < QT * M; e += kThreads) {
         const int ql = e / M;
@@ -162,6 +169,7 @@ topk_small_kernel(ScanArgs a, int k, int metric, int64_t index_base, int tiles, 
     for (int q = lane; q < QT; q += 32) {
         qstate[q] = kNotFull;
         qstate[QT + q] = q0 + q < a.nq ? 0xFFFFu - gthr_inv[q0 + q] + 1u : 0u;  // shared bound + 1 (0x10000 = none)
+        qstate[2 * QT + q] = kNotFull;
     }
     __syncthreads();
     const int64_t gbeg = (blk * kWarpsPB + warp) * gpw;
@@ -184,9 +192,18 @@ topk_small_kernel(ScanArgs a, int k, int metric, int64_t index_base, int tiles, 
             uint64_t* list = lists + q * k;
             uint32_t shr = qstate[QT + q];
             if (refresh) {
-                uint32_t gv;
+                uint32_t gv, sv = 0xFFFFu;
                 asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gv) : "l"(gthr_inv + q0 + q));
-                shr = min(shr, 0xFFFFu - gv + 1u);
+                if (k <= kMaxSlots) {
+                    uint32_t slot = 0;
+                    if (lane < k)
+                        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(slot)
+                                     : "l"(gslot + (q0 + q) * kMaxSlots + lane));
+                    sv = lane < k ? 0xFFFFu - slot : 0u;  // empty slot (0) -> 0xFFFF: no bound
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) sv = max(sv, __shfl_xor_sync(0xffffffffu, sv, off));
+                }
+                shr = min(min(shr, 0xFFFFu - gv + 1u), sv + 1u);
                 qstate[QT + q] = shr;
             }
             // candidates: kv <= min(own k-th, shared bound); equal values may
@@ -205,13 +222,22 @@ topk_small_kernel(ScanArgs a, int k, int metric, int64_t index_base, int tiles, 
             if (__any_sync(0xffffffffu, flag)) {
                 const uint32_t nown = wl_insert_group(list, k, tot[0], tot[1], tot[2], tot[3], flip, nrows, thr,
                                                       (uint64_t)(index_base + g * 8), lane);
-                if (nown < qstate[q]) {
+                const uint32_t nmin = (uint32_t)(list[0] >> 48);  // list[0] != ~0 after an insert
+                if (nown < qstate[q] || (k <= kMaxSlots && nmin < qstate[2 * QT + q])) {
                     __syncwarp();
                     if (lane == 0) {
-                        qstate[q] = nown;
-                        asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gthr_inv + q0 + q),
-                                     "r"(0xFFFFu - nown)
-                                     : "memory");
+                        if (nown < qstate[q]) {
+                            qstate[q] = nown;
+                            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gthr_inv + q0 + q),
+                                         "r"(0xFFFFu - nown)
+                                         : "memory");
+                        }
+                        if (k <= kMaxSlots && nmin < qstate[2 * QT + q]) {
+                            qstate[2 * QT + q] = nmin;
+                            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;"
+                                         ::"l"(gslot + (q0 + q) * kMaxSlots + myslot), "r"(0xFFFFu - nmin)
+                                         : "memory");
+                        }
                     }
                     __syncwarp();
                 }
@@ -251,7 +277,7 @@ cudaError_t launch_qm(const ScanArgs& a, int k, int metric, int64_t index_base, 
     const int tiles = (int)ceil_div(a.nq, QT);
     const int64_t gpw = ceil_div(ceil_div(a.groups, (int64_t)parts * kWarpsPB), 32) * 32;
     const size_t smem = (size_t)QT * M * 2 * sizeof(uint4) + (size_t)kWarpsPB * QT * k * sizeof(uint64_t) +
-                        (size_t)kWarpsPB * 2 * QT * sizeof(uint32_t);
+                        (size_t)kWarpsPB * 3 * QT * sizeof(uint32_t);
     auto kern = topk_small_kernel<QT, M>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)((int64_t)tiles * parts), kThreads, smem, s>>>(a, k, metric, index_base, tiles, gpw, part_keys,
@@ -287,11 +313,12 @@ int topk_small_parts(int64_t n, int m, int64_t nq, int k, int num_sms) {
     return (int)max64(1, min64(max64(blocks / tiles, 1), by_work));
 }
 
-// part_keys: parts*nq*k keys followed by nq u32 shared thresholds (zeroed here).
+// part_keys: parts*nq*k keys followed by nq u32 shared thresholds and nq x 32
+// u32 minima slots (zeroed here).
 cudaError_t launch_topk_small(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
                               uint64_t* part_keys, cudaStream_t s) {
     uint32_t* gthr = reinterpret_cast<uint32_t*>(part_keys + (size_t)parts * a.nq * k);
-    cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)a.nq * sizeof(uint32_t), s);
+    cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)a.nq * (1 + small::kMaxSlots) * sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;
     switch (small::pick_qt(a.nq)) {
         case 8: return small::launch_q<8>(a, k, metric, index_base, parts, part_keys, gthr, s);

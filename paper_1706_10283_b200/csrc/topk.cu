@@ -60,62 +60,57 @@ merge_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int k, uint64
     }
 }
 
-// Merge of many partial lists (the small-batch scan: one list per warp).
+// Merge of many partial lists (the small-batch scan: one list per block).
 // The k smallest list heads are k distinct keys, so the k-th smallest head H
 // bounds the k-th key of the union; only keys <= H can be in the result, and
 // they lie in the k lists whose heads are <= H: at most k*k survivors.
-//   1. heads -> shared memory; k rounds of block argmin give H (no global
-//      loads inside the rounds)
+//   1. heads -> shared memory; k rounds of argmin give H (no global loads
+//      inside the rounds)
 //   2. one coalesced pass over all keys keeps those <= H
-//   3. k rounds of block argmin over the survivors
+//   3. k rounds of argmin over the survivors
 // Used for k <= kFilteredMaxK (k*k survivors fit in shared memory).
 constexpr int kFilteredMaxK = 32;
 
-__device__ __forceinline__ void block_argmin(uint64_t& best, int& bi, uint64_t* wkey, int* wpos) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// One block per query: all threads load the heads and scan the keys (many
+// independent loads in flight), warp 0 alone runs the k-round selections
+// (no block barrier inside a round).
+__device__ __forceinline__ void warp_argmin(uint64_t& best, int& bi) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         const uint64_t o = __shfl_xor_sync(0xffffffffu, best, off);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
         if (o < best || (o == best && (unsigned)oi < (unsigned)bi)) { best = o; bi = oi; }
     }
-    if (lane == 0) { wkey[warp] = best; wpos[warp] = bi; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int t = 1; t < (int)(blockDim.x >> 5); ++t)
-            if (wkey[t] < best || (wkey[t] == best && (unsigned)wpos[t] < (unsigned)bi)) { best = wkey[t]; bi = wpos[t]; }
-        wkey[0] = best;
-        wpos[0] = bi;
-    }
-    __syncthreads();
-    best = wkey[0];
-    bi = wpos[0];
-    __syncthreads();
 }
 
 __global__ void __launch_bounds__(kMergeThreads)
 merge_many_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int k, uint64_t* __restrict__ out) {
     extern __shared__ uint64_t heads[];  // [w] heads, then [k*k] survivors
     uint64_t* surv = heads + w;
+    __shared__ uint64_t sbound;
     __shared__ int count;
-    __shared__ uint64_t wkey[kMergeThreads / 32];
-    __shared__ int wpos[kMergeThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t q = blockIdx.x;
     for (int p = threadIdx.x; p < w; p += blockDim.x) heads[p] = keys[((int64_t)p * nq + q) * k];
     if (threadIdx.x == 0) count = 0;
     __syncthreads();
-    uint64_t bound = ~0ull;
-    for (int r = 0; r < k; ++r) {
-        uint64_t best = ~0ull;
-        int bi = -1;
-        for (int p = threadIdx.x; p < w; p += blockDim.x)
-            if (heads[p] < best) { best = heads[p]; bi = p; }
-        block_argmin(best, bi, wkey, wpos);
-        if (bi < 0 || best == ~0ull) break;  // fewer than k keys in all lists
-        bound = best;
-        if (threadIdx.x == 0) heads[bi] = ~0ull;
-        __syncthreads();
+    if (warp == 0) {
+        uint64_t bound = ~0ull;
+        for (int r = 0; r < k; ++r) {
+            uint64_t best = ~0ull;
+            int bi = -1;
+            for (int p = lane; p < w; p += 32)
+                if (heads[p] < best) { best = heads[p]; bi = p; }
+            warp_argmin(best, bi);
+            if (bi < 0 || best == ~0ull) break;  // fewer than k keys in all lists
+            bound = best;
+            if (lane == 0) heads[bi] = ~0ull;
+            __syncwarp();
+        }
+        if (lane == 0) sbound = bound;
     }
+    __syncthreads();
+    const uint64_t bound = sbound;
     const int64_t total = (int64_t)w * k;
     for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
         const int p = (int)(e / k), rr = (int)(e - (int64_t)p * k);
@@ -126,18 +121,19 @@ merge_many_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int k, u
         }
     }
     __syncthreads();
+    if (warp != 0) return;
     const int n = min(count, k * k);
     for (int r = 0; r < k; ++r) {
         uint64_t best = ~0ull;
         int bi = -1;
-        for (int i = threadIdx.x; i < n; i += blockDim.x)
+        for (int i = lane; i < n; i += 32)
             if (surv[i] < best) { best = surv[i]; bi = i; }
-        block_argmin(best, bi, wkey, wpos);
-        if (threadIdx.x == 0) {
+        warp_argmin(best, bi);
+        if (lane == 0) {
             out[q * k + r] = best;
             if (bi >= 0) surv[bi] = ~0ull;
         }
-        __syncthreads();
+        __syncwarp();
     }
 }
 
@@ -213,8 +209,8 @@ cudaError_t launch_merge(const uint64_t* keys, int w, int64_t nq, int k, uint64_
 
 cudaError_t launch_merge_many(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out, cudaStream_t s) {
     if (nq == 0) return cudaSuccess;
-    if (k > kFilteredMaxK || (size_t)(w + k * k) * sizeof(uint64_t) > 200 * 1024) return launch_merge(keys, w, nq, k, out, s);
     const size_t smem = (size_t)(w + k * k) * sizeof(uint64_t);
+    if (k > kFilteredMaxK || smem > 200 * 1024) return launch_merge(keys, w, nq, k, out, s);
     cudaFuncSetAttribute(merge_many_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     merge_many_kernel<<<(unsigned)nq, kMergeThreads, smem, s>>>(keys, w, nq, k, out);
     return cudaGetLastError();

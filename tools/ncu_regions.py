@@ -1,5 +1,5 @@
 """Group an ncu SASS source page into runs of equal execution count (basic blocks).
-python tools/ncu_regions.py rep.ncu-rep [min_share]"""
+python tools/ncu_regions.py rep.ncu-rep [min_share] [kernel-regex]"""
 import collections
 import csv
 import io
@@ -7,12 +7,14 @@ import re
 import subprocess
 import sys
 
-out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+cmd = ["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source", "sass"]
+if len(sys.argv) > 3:
+    cmd += ["--kernel-name", f"regex:{sys.argv[3]}", "--launch-count", "1"]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
 idx = {h: i for i, h in enumerate(hdr)}
-data = rows[2:]
+data = [r for r in rows[2:] if len(r) == len(hdr) and r[idx["Instructions Executed"]] != "Instructions Executed"]
 thr = float(sys.argv[2]) if len(sys.argv) > 2 else 0.005
 ti = sum(float(r[idx["Instructions Executed"]] or 0) for r in data)
 ts = sum(float(r[idx["Warp Stall Sampling (All Samples)"]] or 0) for r in data)
