@@ -461,6 +461,86 @@ def roofline(variant, n, m, nq, scan_ms, peaks, peak_src, clocks):
                          "gbs": round((n * m // 2 + nq * m * 16) / t / 1e9, 1)}}
 
 
+# ------------------------------------------------------------------ sweep
+SWEEP_Q = (1, 2, 4, 8, 16, 32, 64, 128, 256)
+
+
+def run_sweep(args):
+    """Small-batch regime (SURVEY 8(d) 'sweep'): c5's database (the c2
+    mixture, generated on the GPU by synth/gen_gpu.cu in 1M-row chunks and
+    encoded with the c2 model; N = 1e8 rows = 800 MB of codes, > L2) scanned
+    with top-10 for Q = 1 .. 256 queries of c5.  Reports per Q the scan time,
+    distances/s and the code-stream bandwidth N*M/2 / t (the HBM roofline of
+    small batches: BASELINE north_star 'achieved HBM GB/s for small query
+    batches')."""
+    import torch
+
+    import paper_1706_10283_b200 as bolt
+    from synth import gpu as synth_gpu
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    cfg2, cfg5 = G.CONFIGS["c2"], G.CONFIGS["c5"]
+    n = args.n or cfg5.n
+    train = G.training(cfg2)
+    model = bolt.BoltModel.fit(torch.from_numpy(train).to(dev), cfg2.m,
+                               torch.from_numpy(G.kmeans_init_all(cfg2, len(train))).to(dev),
+                               torch.from_numpy(G.calibration(cfg2, train)).to(dev), cfg2.metrics[0],
+                               iters=cfg2.kmeans_iters)
+    mu = torch.from_numpy(G.c5_means()).to(dev)
+    chunk = 1 << 20
+    codes = torch.empty(bolt.codes_words(n, cfg2.m), dtype=torch.uint32, device=dev)
+    xbuf = torch.empty((chunk, 128), dtype=torch.float32, device=dev)
+    for r0 in range(0, n, chunk):
+        rows = min(chunk, n - r0)
+        synth_gpu.c5_rows(r0, rows, mu, xbuf[:rows])
+        w0 = r0 // 8 * cfg2.m
+        bolt.encode(xbuf[:rows], model.C, out=codes[w0:w0 + bolt.codes_words(rows, cfg2.m)])
+    del xbuf
+    torch.cuda.synchronize()
+    Qall = torch.from_numpy(G.queries(cfg5, max(SWEEP_Q))).to(dev)
+    peaks, peak_src = measured_peaks()
+    stream = torch.cuda.current_stream(dev)
+    code_bytes = n * cfg2.m // 2
+    rows_out = []
+    clk = ClockSampler(0)
+    with clk:
+        for q in SWEEP_Q:
+            ql = bolt.build_quantized_luts(Qall[:q].contiguous(), model.C, cfg2.metrics[0], model.a, model.b)
+            keys = torch.empty((q, 10), dtype=torch.uint64, device=dev)
+            ws = torch.empty(max(bolt.topk_workspace_bytes(n, cfg2.m, q, 10), 8), dtype=torch.uint8, device=dev)
+            variant, parts = bolt.topk_plan(n, cfg2.m, q, 10)
+            for _ in range(args.warmup):
+                bolt.topk(codes, n, ql, 10, cfg2.metrics[0], out=keys, workspace=ws)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                bolt.topk(codes, n, ql, 10, cfg2.metrics[0], out=keys, workspace=ws)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.steps
+            rows_out.append({"q": q, "variant": variant, "parts": parts, "ms": round(ms, 4),
+                             "gdist_s": round(n * q / (ms * 1e-3) / 1e9, 2),
+                             "code_gbs": round(code_bytes / (ms * 1e-3) / 1e9, 1),
+                             "hbm_frac": round(code_bytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4)})
+    r1 = rows_out[0]
+    out = {"metric": METRIC, "value": r1["gdist_s"], "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": r1["ms"], "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "u8",
+           "data": "synthetic (c5: c2 mixture generated on the GPU by Philox4x32-10, SURVEY 8(d))",
+           "config": {"workload": f"sweep: N={n} rows (c5 database, {code_bytes / 1e6:.0f} MB of codes > L2), "
+                                  f"M=16, J=128, squared L2, top-10, Q in {list(SWEEP_Q)}; value = Q=1; step = "
+                                  "scan + top-k (tables prebuilt)", "n_per_gpu": n, "m": 16, "j": 128, "k": 10,
+                      "l2": "codes 800 MB > 126 MB L2 (streamed from HBM every scan)"},
+           "roofline": {"bound": "hbm", "achieved": round(code_bytes / (r1["ms"] * 1e-3) / 1e9, 1),
+                        "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": r1["hbm_frac"], "traffic": None,
+                        "peak_source": f"{peak_src} HBM copy bandwidth", "kernel": f"bolt_topk ({r1['variant']}), Q=1"},
+           "sweep": rows_out, "clocks": clk.summary(),
+           "gpu_launches": args.steps * len(SWEEP_Q) * 3}
+    print(json.dumps(out))
+
+
 # ------------------------------------------------------------- reference
 def run_reference(args):
     """The fp64 CPU oracle as it stands, on the host cores (rank 0 only)."""
@@ -497,7 +577,9 @@ def run_reference(args):
 
 if __name__ == "__main__":
     a = parse()
-    if a.impl == "reference":
+    if a.config == "sweep" and a.impl != "reference":
+        run_sweep(a)
+    elif a.impl == "reference":
         run_reference(a)
     else:
         run_ours(a)

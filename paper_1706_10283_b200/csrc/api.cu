@@ -112,7 +112,8 @@ int64_t tc_prefix_rows(int64_t n) {
 TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     TopkPlan p{};
     int v = variant;
-    if (v == BOLT_VARIANT_AUTO) v = topk_tc_supported(n, m, nq, k) && nq >= 64 ? BOLT_VARIANT_TC : BOLT_VARIANT_PRMT;
+    // auto: tensor cores from 24 queries (sweep crossover, profiles/r1/bench_sweep.json), else PRMT
+    if (v == BOLT_VARIANT_AUTO) v = topk_tc_supported(n, m, nq, k) && nq >= 24 ? BOLT_VARIANT_TC : BOLT_VARIANT_PRMT;
     p.variant = v;
     p.small = v == BOLT_VARIANT_PRMT && topk_small_supported(n, m, nq, k);
     p.parts = v == BOLT_VARIANT_TC ? topk_tc_parts(n, m, nq, k, sms)

@@ -64,6 +64,11 @@ def _c2_means() -> np.ndarray:
     return rng(2, 0).uniform(0.0, 128.0, (1024, 128))
 
 
+def c5_means() -> np.ndarray:
+    """Component means of the c2 mixture, shared by c5's device generator (synth/gen_gpu.cu)."""
+    return _c2_means().astype(np.float32)
+
+
 def _c3_scale() -> np.ndarray:
     return rng(3, 0).uniform(0.1, 2.0, 512)
 

@@ -73,12 +73,22 @@ def test_host_validation(lib):
 
 
 def test_workspace_sizing_host(lib):
-    # the plan is a pure function of the shapes (and SM count): parts * nq * k * 8 bytes
-    for n, m, nq, k in [(10, 8, 4, 10), (1_000_000, 16, 10_000, 10), (10**8, 16, 1, 100)]:
-        ws = lib.bolt_topk_workspace_bytes_ex(n, m, nq, k, 1)
+    # the plan is a pure function of the shapes (and SM count): partial lists
+    # [parts][nq][k] u64, then the shared per-query threshold words: one
+    # (PRMT), 33 (small-batch PRMT kernel, nq < 64 and m in {8,16,32}: k-th
+    # value + 32 minima slots), 3 nq + 1 (tcgen05: k-th value + half-list pairs)
+    for n, m, nq, k, variant in [(10, 8, 4, 10, 1), (1_000_000, 16, 10_000, 10, 1), (10**8, 16, 1, 100, 1),
+                                 (5000, 12, 8, 10, 1), (1_000_000, 16, 10_000, 10, 2), (777, 32, 300, 32, 2)]:
+        ws = lib.bolt_topk_workspace_bytes_ex(n, m, nq, k, variant)
         rv, parts = ctypes.c_int(0), ctypes.c_int(0)
-        assert lib.bolt_topk_plan(n, m, nq, k, 1, ctypes.byref(rv), ctypes.byref(parts)) == 0
-        assert rv.value == 1
-        # partial lists [parts][nq][k] u64 + one u32 shared threshold per query
-        assert ws == (0 if parts.value == 1 else parts.value * nq * k * 8 + nq * 4)
-        assert 1 <= parts.value <= 16384
+        assert lib.bolt_topk_plan(n, m, nq, k, variant, ctypes.byref(rv), ctypes.byref(parts)) == 0
+        assert rv.value == variant
+        p = parts.value
+        if variant == 2:
+            expect = p * nq * k * 8 + (3 * nq + 1) * 4
+        elif nq < 64 and m in (8, 16, 32):
+            expect = p * nq * k * 8 + 33 * nq * 4
+        else:
+            expect = 0 if p == 1 else p * nq * k * 8 + nq * 4
+        assert ws == expect, (n, m, nq, k, variant, p, ws)
+        assert 1 <= p <= 16384

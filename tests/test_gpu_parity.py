@@ -364,6 +364,36 @@ def test_c2_full_size_sampled(bolt, orc):
     np.testing.assert_array_equal(keys[qs], orc.topk(gcodes, qlh[qs], cfg.k, 0))
 
 
+# ------------------------------------- c5 / sweep: device-generated database
+def test_c5_device_rows_sampled(bolt, orc):
+    """c5's rows come from the GPU generator (synth/gen_gpu.cu); a slice far
+    into the 1e8-row database is copied to the host, where the oracle encodes
+    it and scans it for small query batches (the small-batch kernel, several
+    partial lists) and a tcgen05-sized batch."""
+    import torch
+    from synth import gpu as sg
+    cfg2 = G.CONFIGS["c2"]
+    r0, n = 99_900_000, 60_000
+    X = torch.empty((n, 128), dtype=torch.float32, device="cuda")
+    sg.c5_rows(r0, n, dev(G.c5_means()), X)
+    Xh = host(X)
+    assert Xh.min() >= 0 and Xh.max() <= 255 and (Xh == np.rint(Xh)).all()
+    assert 40 < Xh.mean() < 90 and len(np.unique(Xh[:, 0])) > 100  # mixture of clipped normals
+    train = G.training(cfg2, 20_000)
+    C = orc.fit(train, cfg2.m, G.kmeans_init_all(cfg2, len(train)), 3)
+    a, b, _ = orc.fit_quantizer(G.calibration(cfg2, train)[:200], C, 0)
+    codes = bolt.encode(X, dev(C))
+    gcodes = orc.unpack_v1(host(codes), n, cfg2.m)
+    ref, gap = orc.encode(Xh, C, with_gap=True)
+    d = gcodes != ref
+    assert (d <= (gap < 1e-5)).all() and d.sum() <= NEAR_TIE_CAP * d.size
+    Q = G.queries(G.CONFIGS["c5"], 70)
+    for nq, variant in ((1, bolt.VARIANT_AUTO), (5, bolt.VARIANT_AUTO), (70, bolt.VARIANT_TC)):
+        ql = bolt.build_quantized_luts(dev(Q[:nq]), dev(C), 0, float(a), dev(b))
+        keys = host(bolt.topk(codes, n, ql, 10, 0, index_base=r0, variant=variant))
+        np.testing.assert_array_equal(keys, orc.topk(gcodes, host(ql), 10, 0, index_base=r0))
+
+
 # ------------------------------------------------------- offline fit (f1)
 @pytest.mark.parametrize("cfg_name,n", [("c1", 10_000), ("c2", 20_000), ("c4", 5_000)])
 def test_kmeans_gpu_equals_oracle(bolt, orc, cfg_name, n):
