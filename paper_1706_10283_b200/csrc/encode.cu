@@ -110,6 +110,108 @@ encode_kernel(const float* __restrict__ X, int64_t n, int j, int64_t ldx,
     for (int64_t e = threadIdx.x; e < ng * m; e += blockDim.x) dst[e] = stage[e];
 }
 
+// v2 for L = 8 (J/M = 8: c2, c4, c5): 2 rows per thread, the next codebook's
+// 16 floats of the two rows prefetched into registers while the current one
+// is processed (load latency hidden), 256 threads per block.  Same fp32
+// operations in the same order as encode_kernel (bit-identical codes).
+constexpr int kEnc2Threads = 256;
+constexpr int kEnc2Rows = 2;
+constexpr int kEnc2RowsPerBlock = kEnc2Threads * kEnc2Rows;  // 512 = 64 groups
+
+__global__ void __launch_bounds__(kEnc2Threads, 2)
+encode_l8_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const float* __restrict__ C, int m,
+                 uint32_t* __restrict__ codes) {
+    extern __shared__ float4 enc_smem4[];
+    constexpr int L = 8;
+    const int j = m * L;
+    float* cneg = reinterpret_cast<float*>(enc_smem4);  // [m][L][16] negated
+    uint32_t* stage = reinterpret_cast<uint32_t*>(cneg + (size_t)j * kK);  // [64][m]
+    for (int e = threadIdx.x; e < j * kK; e += blockDim.x) {
+        int c = e / (kK * L);
+        int r = e - c * kK * L;
+        int k = r / L;
+        int d = r - k * L;
+        cneg[((size_t)c * L + d) * kK + k] = -C[e];
+    }
+    __syncthreads();
+    // thread t: rows 4*(t/2) + 2*(t%2) + {0,1}: a pair of threads covers 4 rows,
+    // so the 16-bit half-words of a layout-v1 group are built as before
+    const int64_t row0 = (int64_t)blockIdx.x * kEnc2RowsPerBlock + threadIdx.x * kEnc2Rows;
+    const float4* xr[kEnc2Rows];
+    bool valid[kEnc2Rows];
+#pragma unroll
+    for (int r = 0; r < kEnc2Rows; ++r) {
+        valid[r] = row0 + r < n;
+        xr[r] = reinterpret_cast<const float4*>(X + (valid[r] ? (row0 + r) : 0) * ldx);
+    }
+    float4 nx[kEnc2Rows][2];
+#pragma unroll
+    for (int r = 0; r < kEnc2Rows; ++r)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) nx[r][h] = valid[r] ? __ldg(xr[r] + h) : make_float4(0, 0, 0, 0);
+    for (int c = 0; c < m; ++c) {
+        float xv[kEnc2Rows][L];
+#pragma unroll
+        for (int r = 0; r < kEnc2Rows; ++r) {
+            xv[r][0] = nx[r][0].x; xv[r][1] = nx[r][0].y; xv[r][2] = nx[r][0].z; xv[r][3] = nx[r][0].w;
+            xv[r][4] = nx[r][1].x; xv[r][5] = nx[r][1].y; xv[r][6] = nx[r][1].z; xv[r][7] = nx[r][1].w;
+        }
+        if (c + 1 < m) {
+#pragma unroll
+            for (int r = 0; r < kEnc2Rows; ++r)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) nx[r][h] = valid[r] ? __ldg(xr[r] + 2 * (c + 1) + h) : make_float4(0, 0, 0, 0);
+        }
+        float2 d[kEnc2Rows][kK / 2];
+#pragma unroll
+        for (int r = 0; r < kEnc2Rows; ++r)
+#pragma unroll
+            for (int p = 0; p < kK / 2; ++p) d[r][p] = make_float2(0.f, 0.f);
+        const float* cc = cneg + (size_t)c * L * kK;
+#pragma unroll
+        for (int t = 0; t < L; ++t) {
+            const float4* cv = reinterpret_cast<const float4*>(cc + (size_t)t * kK);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                float4 c4 = cv[q];
+                float2 ca = make_float2(c4.x, c4.y), cb = make_float2(c4.z, c4.w);
+#pragma unroll
+                for (int r = 0; r < kEnc2Rows; ++r) {
+                    float2 xx = make_float2(xv[r][t], xv[r][t]);
+                    float2 da = __fadd2_rn(xx, ca);
+                    float2 db = __fadd2_rn(xx, cb);
+                    d[r][2 * q] = __ffma2_rn(da, da, d[r][2 * q]);
+                    d[r][2 * q + 1] = __ffma2_rn(db, db, d[r][2 * q + 1]);
+                }
+            }
+        }
+        uint32_t quarter = 0;  // this thread's 2 rows (8 bits)
+#pragma unroll
+        for (int r = 0; r < kEnc2Rows; ++r) {
+            float best = d[r][0].x;
+            uint32_t arg = 0;
+#pragma unroll
+            for (int p = 0; p < kK / 2; ++p) {
+                if (p > 0 && d[r][p].x < best) { best = d[r][p].x; arg = 2 * p; }
+                if (d[r][p].y < best) { best = d[r][p].y; arg = 2 * p + 1; }
+            }
+            if (!valid[r]) arg = 0;
+            quarter |= arg << (4 * r);
+        }
+        // 4 consecutive threads hold the 8 rows of one group
+        const uint32_t q1 = __shfl_down_sync(0xffffffffu, quarter, 1);
+        const uint32_t q2 = __shfl_down_sync(0xffffffffu, quarter, 2);
+        const uint32_t q3 = __shfl_down_sync(0xffffffffu, quarter, 3);
+        if ((threadIdx.x & 3) == 0) stage[(threadIdx.x >> 2) * m + c] = quarter | (q1 << 8) | (q2 << 16) | (q3 << 24);
+    }
+    __syncthreads();
+    const int64_t g0 = (int64_t)blockIdx.x * kEncGroupsPerBlock;
+    const int64_t groups = ceil_div(n, kRowsPerWord);
+    const int64_t ng = min64(kEncGroupsPerBlock, groups - g0);
+    uint32_t* dst = codes + g0 * m;
+    for (int64_t e = threadIdx.x; e < ng * m; e += blockDim.x) dst[e] = stage[e];
+}
+
 __global__ void pack_kernel(const uint8_t* __restrict__ flat, int64_t n, int m,
                             uint32_t* __restrict__ codes) {
     int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -143,7 +245,11 @@ cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const f
     size_t smem = (size_t)j * kK * sizeof(float) + (size_t)kEncGroupsPerBlock * m * sizeof(uint32_t);
     bool vec = (L % 4 == 0) && (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
     int64_t blocks = ceil_div(n, kEncRowsPerBlock);
-    if (vec) {
+    if (vec && L == 8) {
+        static_assert(kEnc2RowsPerBlock == kEncRowsPerBlock, "same 64-group staging");
+        cudaFuncSetAttribute(encode_l8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        encode_l8_kernel<<<(unsigned)blocks, kEnc2Threads, smem, s>>>(X, n, ldx, C, m, codes);
+    } else if (vec) {
         cudaFuncSetAttribute(encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         encode_kernel<true><<<(unsigned)blocks, kEncThreads, smem, s>>>(X, n, j, ldx, C, m, codes);
     } else {

@@ -23,6 +23,19 @@ __device__ __forceinline__ uint32_t op(uint32_t a, uint32_t b) {
     if (OP == 11) asm volatile("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
     if (OP == 12) asm volatile("mad.lo.u32 %0, %1, 8, -96;" : "=r"(d) : "r"(a));
     if (OP == 13) asm volatile("shl.b32 %0, %1, 3;" : "=r"(d) : "r"(a));
+    if (OP == 14) asm volatile("fma.rn.f32 %0, %1, %2, %1;" : "=r"(d) : "r"(a), "r"(b));
+    if (OP == 15) {
+        float2 x = make_float2(__uint_as_float(a), __uint_as_float(a ^ 1));
+        float2 y = make_float2(__uint_as_float(b), __uint_as_float(b));
+        float2 z = __ffma2_rn(x, y, x);
+        d = __float_as_uint(z.x) ^ __float_as_uint(z.y);
+    }
+    if (OP == 16) {
+        float2 x = make_float2(__uint_as_float(a), __uint_as_float(a ^ 1));
+        float2 y = make_float2(__uint_as_float(b), __uint_as_float(b));
+        float2 z = __fadd2_rn(x, y);
+        d = __float_as_uint(z.x) ^ __float_as_uint(z.y);
+    }
     return d;
 }
 __device__ __forceinline__ uint32_t lop(uint32_t a, uint32_t b) {
@@ -89,5 +102,8 @@ int main() {
     run<11>("add.f16x2", out, cyc);
     run<12>("mad imm 8,-96", out, cyc);
     run<13>("shl imm", out, cyc);
+    run<14>("fma.f32", out, cyc);
+    run<15>("ffma2 (+lop)", out, cyc);
+    run<16>("fadd2 (+lop)", out, cyc);
     return 0;
 }
