@@ -88,17 +88,22 @@ constexpr int kMmaWarp = kProdWarps + kEpiWarps;
 constexpr int kThreads = (kMmaWarp + 1) * 32;
 constexpr int kMaxTopk = 32;
 constexpr int kPrefetch = 3;             // tiles of code words in flight per producer thread
-constexpr int kScratchStride = 20;       // u32 words per epilogue thread: 32 u16 values + pad
+// u32 words of shared scratch per epilogue thread: top-k parks 32 u16 values
+// (80-byte rows: 16-byte aligned, conflict-free); full output stages a 32-row x
+// 128-byte block per warp (4 KB)
+constexpr int kScratchStrideTopk = 20;
+constexpr int kScratchStrideFull = 32;
 
-template <int M>
+template <int M, bool kFull = false>
 struct Cfg {
+    static constexpr int SCRATCH_STRIDE = kFull ? kScratchStrideFull : kScratchStrideTopk;
     static constexpr int K = 16 * M;                      // bytes per row
     static constexpr int N = 256;                         // vectors per MMA tile (pair)
     static constexpr int NH = N / 2;                      // vectors per CTA (its half of B)
     static constexpr int A_BYTES = kQM * K;
     static constexpr int B_BYTES = NH * K;                // one stage of this CTA's half of B
-    static constexpr int SCRATCH_BYTES = kEpilogue * kScratchStride * 4;
-    static constexpr int STAGES_RAW = (220 * 1024 - A_BYTES - SCRATCH_BYTES) / B_BYTES;
+    static constexpr int SCRATCH_BYTES = kEpilogue * SCRATCH_STRIDE * 4;
+    static constexpr int STAGES_RAW = (227 * 1024 - 256 - A_BYTES - SCRATCH_BYTES) / B_BYTES;
     static constexpr int STAGES = STAGES_RAW > 5 ? 5 : STAGES_RAW;
     static_assert(STAGES >= 2, "shared memory too small for a double-buffered B tile");
     static constexpr int KSTEPS = K / 32;
@@ -335,7 +340,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
 #ifndef BOLT_XMODE
     xmode = 0;  // diagnostic stage switches exist only in libbolt_x.so (tools/)
 #endif
-    using C = Cfg<M>;
+    using C = Cfg<M, (kOut != 0)>;
     constexpr int S = C::STAGES;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sA = smem;
@@ -472,7 +477,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
         const int half = warp >> 2;                // column half of the tile
         const int q = quad * 32 + lane;            // query row of this CTA
         constexpr int kCols = C::N / 2;
-        uint32_t* scratch = scratch_all + threadIdx.x * kScratchStride;
+        uint32_t* scratch = scratch_all + threadIdx.x * C::SCRATCH_STRIDE;
         RegList<KMAX> list;
         list.init(k);
         // Thresholds in kv' units.  own = k-th key of this list; shared =
@@ -532,49 +537,65 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             const long long tp0 = BOLT_CLOCK();
             if (xmode & 1) continue;  // diagnostic: load + release only
             if constexpr (kOut != 0) {
-                // full output, swapped roles: this thread = database vector (TMEM
-                // lane), registers = 128 consecutive queries of its output row
-                const int64_t vi = vbeg + (int64_t)tile * C::N + rank * C::NH + quad * 32 + lane;
+                // Full output, swapped roles: this thread = database vector (TMEM
+                // lane), registers = 128 consecutive queries of its output row.
+                // Each 128-byte row segment (32 fp32 / 64 u16 queries) is written
+                // whole: the warp stages its 32 rows x 128 B block in shared
+                // memory (16-byte units XOR-swizzled by row, conflict-free both
+                // ways) and reads it back so that each 16-byte global store
+                // instruction covers 4 rows x 128 contiguous bytes.
+                const int64_t vrow0 = vbeg + (int64_t)tile * C::N + rank * C::NH + quad * 32;  // warp's first row
                 const int64_t qb = (int64_t)tq * 2 * kQM + half * kCols;  // first query of this warp
-                if (vi < vend) {
-                    if (kOut == 1) {
-                        uint16_t* row = static_cast<uint16_t*>(fo.out) + vi * fo.ldo + qb;
+                uint4* stg = reinterpret_cast<uint4*>(scratch_all) + (warp & 7) * 256;  // 32 rows x 8 units
+                constexpr int kEsz = kOut == 1 ? 2 : 4;
+                constexpr int kQPU = 16 / kEsz;         // queries per 16-byte unit
+                constexpr int kSeg = 8 * kQPU;          // queries per 128-byte segment
 #pragma unroll
-                        for (int c = 0; c < 4; ++c)
+                for (int sg = 0; sg < kCols / kSeg; ++sg) {
+                    // this lane's row: 8 units of the segment
 #pragma unroll
-                            for (int i = 0; i < 16; i += 4) {
-                                const int64_t qq = qb + c * 32 + 2 * i;  // 8 queries: qq .. qq+7
-                                if (fo.vec && qq + 8 <= a.nq)
-                                    *reinterpret_cast<uint4*>(row + c * 32 + 2 * i) =
-                                        make_uint4(p[c][i], p[c][i + 1], p[c][i + 2], p[c][i + 3]);
-                                else
+                    for (int f = 0; f < 8; ++f) {
+                        uint4 u;
+                        if (kOut == 1) {
+                            const int c = (sg * kSeg + f * 8) / 32, i = ((sg * kSeg + f * 8) % 32) / 2;
+                            u = make_uint4(p[c][i], p[c][i + 1], p[c][i + 2], p[c][i + 3]);
+                        } else {
+                            const int c = (sg * kSeg + f * 4) / 32, i = ((sg * kSeg + f * 4) % 32) / 2;
+                            float fv[4];
 #pragma unroll
-                                    for (int e = 0; e < 8; ++e)
-                                        if (qq + e < a.nq)
-                                            row[c * 32 + 2 * i + e] = (uint16_t)(p[c][i + e / 2] >> (16 * (e & 1)));
-                            }
-                    } else {
-                        float* row = static_cast<float*>(fo.out) + vi * fo.ldo + qb;
-#pragma unroll
-                        for (int c = 0; c < 4; ++c)
-#pragma unroll
-                            for (int i = 0; i < 16; i += 2) {
+                            for (int e = 0; e < 4; ++e) {
                                 // exact u16 -> fp32: bits 0x4B00xxxx = 2^23 + x, minus 2^23
-                                float f[4];
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    const uint32_t bits = __byte_perm(p[c][i + e / 2], 0x4B000000u, (e & 1) ? 0x7632 : 0x7610);
-                                    f[e] = fmaf(__uint_as_float(bits) - 8388608.0f, fo.inv_a, fo.b_sum);
-                                }
-                                const int64_t qq = qb + c * 32 + 2 * i;  // 4 queries: qq .. qq+3
-                                if (fo.vec && qq + 4 <= a.nq)
-                                    *reinterpret_cast<float4*>(row + c * 32 + 2 * i) = make_float4(f[0], f[1], f[2], f[3]);
-                                else
-#pragma unroll
-                                    for (int e = 0; e < 4; ++e)
-                                        if (qq + e < a.nq) row[c * 32 + 2 * i + e] = f[e];
+                                const uint32_t bits = __byte_perm(p[c][i + e / 2], 0x4B000000u, (e & 1) ? 0x7632 : 0x7610);
+                                fv[e] = fmaf(__uint_as_float(bits) - 8388608.0f, fo.inv_a, fo.b_sum);
                             }
+                            u = make_uint4(__float_as_uint(fv[0]), __float_as_uint(fv[1]), __float_as_uint(fv[2]),
+                                           __float_as_uint(fv[3]));
+                        }
+                        stg[lane * 8 + (f ^ (lane & 7))] = u;
                     }
+                    __syncwarp();
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int r = 4 * i + (lane >> 3), f = lane & 7;
+                        const uint4 u = stg[r * 8 + (f ^ (r & 7))];
+                        const int64_t vi = vrow0 + r;
+                        const int64_t q = qb + sg * kSeg + f * kQPU;  // first query of the unit
+                        if (vi < vend) {
+                            char* dst = static_cast<char*>(fo.out) + (vi * fo.ldo + q) * kEsz;
+                            if (fo.vec && q + kQPU <= a.nq) {
+                                *reinterpret_cast<uint4*>(dst) = u;
+                            } else {
+                                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                                for (int e = 0; e < kQPU; ++e)
+                                    if (q + e < a.nq) {
+                                        if (kOut == 1) reinterpret_cast<uint16_t*>(dst)[e] = (uint16_t)(w[e / 2] >> (16 * (e & 1)));
+                                        else reinterpret_cast<uint32_t*>(dst)[e] = w[e];
+                                    }
+                            }
+                        }
+                    }
+                    __syncwarp();
                 }
                 continue;
             }
@@ -729,7 +750,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
 template <int M, bool kDot, int KMAX, int kOut = 0>
 cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, uint64_t* part_keys,
                       uint32_t* gthr, cudaStream_t s, bool init_thr, FullOut fo = FullOut{}) {
-    using C = Cfg<M>;
+    using C = Cfg<M, (kOut != 0)>;
     const int tiles_q = (int)ceil_div(a.nq, 2 * kQM);
     const int64_t vpp = ceil_div(ceil_div(a.n, rparts), 8) * 8;
     auto kern = topk_tc_kernel<M, kDot, KMAX, kOut>;
