@@ -29,6 +29,7 @@
 // Shared-memory operand layout (both K-major, SWIZZLE_NONE): the 16-byte
 // chunk j of row r lives at j * (rows * 16) + (r / 8) * 128 + (r % 8) * 16,
 // so SBO (next 8 rows) = 128 B and LBO (next 16-byte K chunk) = rows * 16 B.
+#include <cuda.h>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -331,12 +332,19 @@ struct FullOut {
     int64_t ldo;
     float inv_a, b_sum;
     int vec;  // rows 16 B aligned: vector stores
+    int tma;  // store the staged blocks with TMA (omap valid; partitions are whole 256-row tiles)
 };
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem), "r"(x), "r"(y)
+                 : "memory");
+}
 
 template <int M, bool kDot, int KMAX, int kOut = 0>
 __global__ void __launch_bounds__(kThreads, 1)
 topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, uint64_t* __restrict__ part_keys,
-               uint32_t* __restrict__ gthr_inv, int xmode, FullOut fo) {
+               uint32_t* __restrict__ gthr_inv, int xmode, FullOut fo, const __grid_constant__ CUtensorMap omap) {
 #ifndef BOLT_XMODE
     xmode = 0;  // diagnostic stage switches exist only in libbolt_x.so (tools/)
 #endif
@@ -573,6 +581,20 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                         }
                         stg[lane * 8 + (f ^ (lane & 7))] = u;
                     }
+                    if (fo.tma) {
+                        // one TMA store of the warp's 32 x 128-byte block (the staging
+                        // layout is the tensor map's 128-byte swizzle)
+                        fence_proxy_async();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&omap, smem_u32(stg), (int)(qb + sg * kSeg), (int)vrow0);
+                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                            // the staging block is rewritten by the next segment
+                            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        }
+                        __syncwarp();
+                        continue;
+                    }
                     __syncwarp();
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
@@ -683,6 +705,8 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                 }
             }
         }
+        if (kOut != 0 && fo.tma && lane == 0)  // TMA stores of this warp complete before exit
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         if (kOut == 0 && q0 + q < a.nq) {
             uint64_t* dst = part_keys + ((int64_t)(2 * part + half) * a.nq + q0 + q) * k;
 #pragma unroll
@@ -749,10 +773,13 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
 
 template <int M, bool kDot, int KMAX, int kOut = 0>
 cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, uint64_t* part_keys,
-                      uint32_t* gthr, cudaStream_t s, bool init_thr, FullOut fo = FullOut{}) {
+                      uint32_t* gthr, cudaStream_t s, bool init_thr, FullOut fo = FullOut{},
+                      const CUtensorMap& omap = CUtensorMap{}) {
     using C = Cfg<M, (kOut != 0)>;
     const int tiles_q = (int)ceil_div(a.nq, 2 * kQM);
-    const int64_t vpp = ceil_div(ceil_div(a.n, rparts), 8) * 8;
+    // full output with TMA stores: partitions of whole 256-vector tiles, so that
+    // a tile's 256 rows never reach into the next partition
+    const int64_t vpp = fo.tma ? ceil_div(ceil_div(a.n, rparts), C::N) * C::N : ceil_div(ceil_div(a.n, rparts), 8) * 8;
     auto kern = topk_tc_kernel<M, kDot, KMAX, kOut>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaLaunchConfig_t cfg{};
@@ -778,14 +805,31 @@ cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, 
                                  : cudaMemsetAsync(gthr + hoff, 0, (size_t)a.nq * 2 * sizeof(uint32_t), s);
         if (e != cudaSuccess) return e;
     }
-    return cudaLaunchKernelEx(&cfg, kern, a, k, index_base, vpp, tiles_q, part_keys, gthr, xmode, fo);
+    return cudaLaunchKernelEx(&cfg, kern, a, k, index_base, vpp, tiles_q, part_keys, gthr, xmode, fo, omap);
 }
 
 // full [n][nq] output: u16 sums (out32 == nullptr) or fp32 dequantised
 template <int M>
-cudaError_t launch_full_m(const ScanArgs& a, int rparts, FullOut fo, bool f32, cudaStream_t s) {
-    return f32 ? launch_mk<M, false, 4, 2>(a, 1, 0, rparts, nullptr, nullptr, s, false, fo)
-               : launch_mk<M, false, 4, 1>(a, 1, 0, rparts, nullptr, nullptr, s, false, fo);
+cudaError_t launch_full_m(const ScanArgs& a, int rparts, FullOut fo, const CUtensorMap& omap, bool f32,
+                          cudaStream_t s) {
+    return f32 ? launch_mk<M, false, 4, 2>(a, 1, 0, rparts, nullptr, nullptr, s, false, fo, omap)
+               : launch_mk<M, false, 4, 1>(a, 1, 0, rparts, nullptr, nullptr, s, false, fo, omap);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
 }
 
 template <int M>
@@ -824,11 +868,25 @@ cudaError_t launch_scan_tc(const ScanArgs& a, uint16_t* out16, float* out32, int
     void* out = out32 ? static_cast<void*>(out32) : static_cast<void*>(out16);
     const int esz = out32 ? 4 : 2;
     const int vec = (reinterpret_cast<uintptr_t>(out) % 16 == 0) && ((ldo * esz) % 16 == 0);
-    tc::FullOut fo{out, ldo, inv_a, b_sum, vec};
+    // TMA stores of the staged 32-row x 128-byte blocks: a 2-D tensor map over
+    // out [n][nq] (row stride ldo) with the 128-byte swizzle of the staging
+    // layout; the hardware clips rows >= n and queries >= nq
+    CUtensorMap omap{};
+    int tma = 0;
+    if (vec && tc::encode_tiled()) {
+        const cuuint64_t dims[2] = {(cuuint64_t)a.nq, (cuuint64_t)a.n};
+        const cuuint64_t strides[1] = {(cuuint64_t)(ldo * esz)};
+        const cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 32u};
+        const cuuint32_t estr[2] = {1u, 1u};
+        tma = tc::encode_tiled()(&omap, out32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, out,
+                             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    tc::FullOut fo{out, ldo, inv_a, b_sum, vec, tma};
     switch (a.m) {
-        case 8: return tc::launch_full_m<8>(a, rparts, fo, out32 != nullptr, s);
-        case 16: return tc::launch_full_m<16>(a, rparts, fo, out32 != nullptr, s);
-        case 32: return tc::launch_full_m<32>(a, rparts, fo, out32 != nullptr, s);
+        case 8: return tc::launch_full_m<8>(a, rparts, fo, omap, out32 != nullptr, s);
+        case 16: return tc::launch_full_m<16>(a, rparts, fo, omap, out32 != nullptr, s);
+        case 32: return tc::launch_full_m<32>(a, rparts, fo, omap, out32 != nullptr, s);
         default: return cudaErrorInvalidValue;
     }
 }
