@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--nq", type=int, default=0, help="override queries (debug)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--e2e-chunks", type=int, default=8, help="row blocks of the copy/compute-overlapped host search")
     p.add_argument("--no-graph", action="store_true", help="time the step eagerly instead of a CUDA graph")
     return p.parse_args()
 
@@ -339,7 +340,7 @@ def run_ours(args):
                "h2d_bytes_per_step": int(X.nbytes + Q.nbytes), "d2h_bytes_per_step": int(out.numel() * out.element_size()),
                "ms_per_step": round(e_ms, 3), "api": "bolt.encode / build_quantized_luts / scan* (pinned host buffers)"}
     elif args.e2e_steps > 0:
-        hs = bolt.HostSearch(n, cfg.j, cfg.m, nq, k, device=dev)
+        hs = bolt.HostSearch(n, cfg.j, cfg.m, nq, k, device=dev, chunks=args.e2e_chunks)
         Xh = torch.from_numpy(X).pin_memory()
         Qh = torch.from_numpy(Q).pin_memory()
         kh = torch.empty((nq, k), dtype=torch.uint64).pin_memory()
@@ -370,7 +371,8 @@ def run_ours(args):
         e2e = {"value": round(dists / (e_ms * 1e-3) / 1e9, 4), "unit": UNIT,
                "h2d_bytes_per_step": int(X.nbytes + Q.nbytes),
                "d2h_bytes_per_step": int(nq * k * 8), "ms_per_step": round(e_ms, 3),
-               "api": "bolt_search_host (pinned host X, Q -> keys)"}
+               "api": f"bolt_search_host{'_pipelined' if args.e2e_chunks > 1 else ''} (pinned host X, Q -> keys"
+                      f"{f'; X in {args.e2e_chunks} blocks overlapped with encode + scan' if args.e2e_chunks > 1 else ''})"}
 
     # --- roofline of the dominant kernel (scan + fused top-k, or the full-output scan)
     peaks, peak_src = measured_peaks()

@@ -198,6 +198,20 @@ BOLT_API bolt_status bolt_search_host(const float* X_host, int64_t n, int j, con
                              const float* b, int k, uint64_t* keys_host, void* ws,
                              size_t ws_bytes, bolt_stream_t stream);
 
+/* Same search with the host->device copy of X overlapped with the compute:
+ * X crosses in `chunks` row blocks (boundaries at multiples of 256 rows) on
+ * copy_stream, while `stream` encodes each block as soon as it has landed and
+ * runs its top-k (global indices); the block lists are then merged (the
+ * result equals bolt_search_host bit for bit).  copy_stream first waits for
+ * the work already enqueued on `stream`.  1 <= chunks <= 64.
+ * ws >= bolt_search_host_pipelined_workspace_bytes(...) device bytes. */
+BOLT_API size_t bolt_search_host_pipelined_workspace_bytes(int64_t n, int j, int m, int64_t nq, int k, int chunks);
+BOLT_API bolt_status bolt_search_host_pipelined(const float* X_host, int64_t n, int j, const float* Q_host,
+                                                int64_t nq, const float* C, int m, bolt_metric metric, float a,
+                                                const float* b, int k, uint64_t* keys_host, void* ws,
+                                                size_t ws_bytes, int chunks, bolt_stream_t stream,
+                                                bolt_stream_t copy_stream);
+
 /* ----------------------------------------------- offline fit */
 /* k-means codebooks (R8): per subspace, centroids start at rows
  * init[c][0..15] of train, exactly `iters` Lloyd iterations in fp64

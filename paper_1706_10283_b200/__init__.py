@@ -205,13 +205,20 @@ def keys_split(keys: torch.Tensor, metric):
 
 # --------------------------------------------------------- end-to-end (host)
 class HostSearch:
-    """Host-buffer search through bolt_search_host: H2D of X and Q, encode,
-    fused tables, top-k, D2H of the keys, all enqueued on one stream."""
+    """Host-buffer search: H2D of X and Q, encode, fused tables, top-k, D2H of
+    the keys.  chunks == 1: bolt_search_host, everything on one stream;
+    chunks > 1: bolt_search_host_pipelined, X crossing PCIe in row blocks on a
+    side stream while the current stream encodes and scans the blocks that
+    have landed (same keys)."""
 
-    def __init__(self, n: int, j: int, m: int, nq: int, k: int, device=None):
-        self.n, self.j, self.m, self.nq, self.k = n, j, m, nq, k
+    def __init__(self, n: int, j: int, m: int, nq: int, k: int, device=None, chunks: int = 1):
+        self.n, self.j, self.m, self.nq, self.k, self.chunks = n, j, m, nq, k, chunks
         self.device = torch.device(device or "cuda")
-        wsb = int(_lib.load().bolt_search_host_workspace_bytes(n, j, m, nq, k))
+        if chunks > 1:
+            wsb = int(_lib.load().bolt_search_host_pipelined_workspace_bytes(n, j, m, nq, k, chunks))
+            self.copy_stream = torch.cuda.Stream(self.device)
+        else:
+            wsb = int(_lib.load().bolt_search_host_workspace_bytes(n, j, m, nq, k))
         self.workspace = torch.empty(wsb, dtype=torch.uint8, device=self.device)
 
     def __call__(self, X_host: torch.Tensor, Q_host: torch.Tensor, C: torch.Tensor, metric, a: float,
@@ -223,10 +230,16 @@ class HostSearch:
             raise TypeError("keys_host must be a uint64 host tensor")
         _cuda(C, "C", torch.float32)
         _cuda(b, "b", torch.float32)
-        _lib.call("bolt_search_host", X_host.data_ptr(), self.n, self.j, Q_host.data_ptr(), self.nq,
-                  C.data_ptr(), self.m, _metric(metric), float(a), b.data_ptr(), self.k,
-                  keys_host.data_ptr(), self.workspace.data_ptr(), self.workspace.numel(),
-                  _stream(self.device))
+        if self.chunks > 1:
+            _lib.call("bolt_search_host_pipelined", X_host.data_ptr(), self.n, self.j, Q_host.data_ptr(), self.nq,
+                      C.data_ptr(), self.m, _metric(metric), float(a), b.data_ptr(), self.k,
+                      keys_host.data_ptr(), self.workspace.data_ptr(), self.workspace.numel(), self.chunks,
+                      _stream(self.device), self.copy_stream.cuda_stream)
+        else:
+            _lib.call("bolt_search_host", X_host.data_ptr(), self.n, self.j, Q_host.data_ptr(), self.nq,
+                      C.data_ptr(), self.m, _metric(metric), float(a), b.data_ptr(), self.k,
+                      keys_host.data_ptr(), self.workspace.data_ptr(), self.workspace.numel(),
+                      _stream(self.device))
         return keys_host
 
 

@@ -43,6 +43,9 @@ SIGNATURES = {
     "bolt_keys_split": ([_P, _I64, _I32, _P, _P, _P], _I32),
     "bolt_search_host_workspace_bytes": ([_I64, _I32, _I32, _I64, _I32], _SZ),
     "bolt_search_host": ([_P, _I64, _I32, _P, _I64, _P, _I32, _I32, _F32, _P, _I32, _P, _P, _SZ, _P], _I32),
+    "bolt_search_host_pipelined_workspace_bytes": ([_I64, _I32, _I32, _I64, _I32, _I32], _SZ),
+    "bolt_search_host_pipelined": ([_P, _I64, _I32, _P, _I64, _P, _I32, _I32, _F32, _P, _I32, _P, _P, _SZ, _I32,
+                                    _P, _P], _I32),
     "bolt_kmeans_workspace_bytes": ([_I64, _I32, _I32], _SZ),
     "bolt_kmeans": ([_P, _I64, _I32, _I64, _I32, _P, _I32, _P, _P, _SZ, _P], _I32),
     "bolt_calibrate_workspace_bytes": ([_I64, _I32], _SZ),

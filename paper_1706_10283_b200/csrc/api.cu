@@ -467,6 +467,99 @@ bolt_status bolt_search_host(const float* X_host, int64_t n, int j, const float*
 }
 
 // ------------------------------------------------------------------- fit
+// Pipelined host search: the database crosses PCIe in `chunks` row blocks on
+// copy_stream while `stream` encodes and scans the blocks already resident
+// (per-block top-k with the global index base), so the compute hides under the
+// host->device copy; the block lists are merged at the end (exact: total key
+// order).  Events are created per call and released after enqueueing.
+static int64_t chunk_row(int64_t n, int chunks, int i) {
+    // boundaries at multiples of 256 rows (whole layout-v1 groups and scan tiles)
+    const int64_t per = ceil_div(ceil_div(n, chunks), 256) * 256;
+    return min64(n, per * i);
+}
+
+size_t bolt_search_host_pipelined_workspace_bytes(int64_t n, int j, int m, int64_t nq, int k, int chunks) {
+    if (n < 0 || nq < 0 || j < 1 || m < 1 || m > kMaxM || k < 1 || k > kMaxK || chunks < 1 || chunks > 64) return 0;
+    size_t s = 0;
+    s += align256((size_t)n * j * sizeof(float));
+    s += align256((size_t)nq * j * sizeof(float));
+    s += align256((size_t)ceil_div(n, 8) * m * sizeof(uint32_t));
+    s += align256((size_t)nq * m * kK);
+    s += align256((size_t)chunks * nq * k * sizeof(uint64_t));
+    s += align256((size_t)nq * k * sizeof(uint64_t));
+    size_t tws = 0;
+    for (int i = 0; i < chunks; ++i) {
+        const int64_t r = chunk_row(n, chunks, i + 1) - chunk_row(n, chunks, i);
+        if (r > 0) tws = tws > bolt_topk_workspace_bytes(r, m, nq, k) ? tws : bolt_topk_workspace_bytes(r, m, nq, k);
+    }
+    return s + align256(tws);
+}
+
+bolt_status bolt_search_host_pipelined(const float* X_host, int64_t n, int j, const float* Q_host, int64_t nq,
+                                       const float* C, int m, bolt_metric metric, float a, const float* b, int k,
+                                       uint64_t* keys_host, void* ws, size_t ws_bytes, int chunks,
+                                       bolt_stream_t stream, bolt_stream_t copy_stream) {
+    TRY(check_jm(j, m));
+    if (n < 1 || nq < 0) return fail(BOLT_E_SHAPE, "n must be >= 1, nq >= 0");
+    if (k < 1 || k > kMaxK) return fail(BOLT_E_SHAPE, "k = %d outside 1..128", k);
+    if (chunks < 1 || chunks > 64) return fail(BOLT_E_RANGE, "chunks = %d outside 1..64", chunks);
+    if (!(a > 0.f)) return fail(BOLT_E_RANGE, "a must be > 0");
+    if (nq == 0) return BOLT_OK;
+    if (!X_host || !Q_host || !C || !b || !keys_host || !ws) return fail(BOLT_E_NULL, "bolt_search_host_pipelined: NULL pointer");
+    const size_t need = bolt_search_host_pipelined_workspace_bytes(n, j, m, nq, k, chunks);
+    if (ws_bytes < need) return fail(BOLT_E_WORKSPACE, "workspace of %zu bytes required, %zu given", need, ws_bytes);
+    if (!aligned(ws, 256)) return fail(BOLT_E_ALIGN, "workspace must be 256-byte aligned");
+    DevInfo d;
+    TRY(device_info(&d));
+    cudaStream_t s = (cudaStream_t)stream, cs = (cudaStream_t)copy_stream;
+    char* p = static_cast<char*>(ws);
+    float* Xd = reinterpret_cast<float*>(p); p += align256((size_t)n * j * sizeof(float));
+    float* Qd = reinterpret_cast<float*>(p); p += align256((size_t)nq * j * sizeof(float));
+    uint32_t* codes = reinterpret_cast<uint32_t*>(p); p += align256((size_t)ceil_div(n, 8) * m * sizeof(uint32_t));
+    uint8_t* ql = reinterpret_cast<uint8_t*>(p); p += align256((size_t)nq * m * kK);
+    uint64_t* parts = reinterpret_cast<uint64_t*>(p); p += align256((size_t)chunks * nq * k * sizeof(uint64_t));
+    uint64_t* keys = reinterpret_cast<uint64_t*>(p); p += align256((size_t)nq * k * sizeof(uint64_t));
+    void* tws = p;
+    const size_t tws_bytes = need - (size_t)(p - static_cast<char*>(ws));
+    cudaEvent_t start, ev[64];
+    TRY(cuda_status(cudaEventCreateWithFlags(&start, cudaEventDisableTiming), "event"));
+    // the copies may only overwrite Xd once everything enqueued on `stream` before this call is done
+    TRY(cuda_status(cudaEventRecord(start, s), "event record"));
+    TRY(cuda_status(cudaStreamWaitEvent(cs, start, 0), "stream wait"));
+    cudaEventDestroy(start);
+    // Q first on the copy stream: host->device copies share one DMA queue, so a
+    // Q copy behind the X blocks would hold the tables (and every block's scan)
+    // until all of X had landed
+    cudaEvent_t evq;
+    TRY(cuda_status(cudaEventCreateWithFlags(&evq, cudaEventDisableTiming), "event"));
+    TRY(cuda_status(cudaMemcpyAsync(Qd, Q_host, (size_t)nq * j * sizeof(float), cudaMemcpyHostToDevice, cs), "H2D Q"));
+    TRY(cuda_status(cudaEventRecord(evq, cs), "event record"));
+    int used = 0;
+    for (int i = 0; i < chunks; ++i) {
+        const int64_t r0 = chunk_row(n, chunks, i), r1 = chunk_row(n, chunks, i + 1);
+        if (r1 <= r0) break;
+        TRY(cuda_status(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "event"));
+        TRY(cuda_status(cudaMemcpyAsync(Xd + r0 * j, X_host + r0 * j, (size_t)(r1 - r0) * j * sizeof(float),
+                                        cudaMemcpyHostToDevice, cs), "H2D X"));
+        TRY(cuda_status(cudaEventRecord(ev[i], cs), "event record"));
+        used = i + 1;
+    }
+    TRY(cuda_status(cudaStreamWaitEvent(s, evq, 0), "stream wait"));
+    cudaEventDestroy(evq);
+    TRY(bolt_build_quantized_luts(Qd, nq, j, j, C, m, metric, a, b, ql, nullptr, stream));
+    for (int i = 0; i < used; ++i) {
+        const int64_t r0 = chunk_row(n, chunks, i), r1 = chunk_row(n, chunks, i + 1);
+        TRY(cuda_status(cudaStreamWaitEvent(s, ev[i], 0), "stream wait"));
+        cudaEventDestroy(ev[i]);
+        uint32_t* cw = codes + (r0 / 8) * m;
+        TRY(bolt_encode(Xd + r0 * j, r1 - r0, j, j, C, m, cw, stream));
+        TRY(bolt_topk(cw, r1 - r0, m, ql, nq, k, metric, r0, used == 1 ? keys : parts + (size_t)i * nq * k, tws,
+                      tws_bytes, stream));
+    }
+    if (used > 1) TRY(bolt_topk_merge(parts, used, nq, k, keys, stream));
+    return cuda_status(cudaMemcpyAsync(keys_host, keys, (size_t)nq * k * sizeof(uint64_t), cudaMemcpyDeviceToHost, s), "D2H keys");
+}
+
 size_t bolt_kmeans_workspace_bytes(int64_t n, int j, int m) {
     if (n < 1 || j < 1 || m < 1 || m > kMaxM || j % m) return 0;
     return kmeans_ws_bytes(n, j, m);

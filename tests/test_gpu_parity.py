@@ -337,6 +337,27 @@ def test_search_host_matches_device_path(bolt, orc, c1_model):
     np.testing.assert_array_equal(keys_h.numpy(), host(bolt.topk(codes, cfg.n, ql, 10, 0)))
 
 
+@pytest.mark.parametrize("chunks", [2, 3, 7])
+def test_host_search_pipelined(bolt, orc, c1_model, chunks):
+    """The copy/compute-overlapped host search returns the same keys as the
+    single-stream one (block top-k lists merged; ragged last block)."""
+    cfg, X, C, params = c1_model
+    a, b, _ = params[0]
+    Q = G.queries(cfg)
+    Xh, Qh = torch.from_numpy(X).pin_memory(), torch.from_numpy(Q).pin_memory()
+    k1 = torch.empty((cfg.nq, 10), dtype=torch.uint64).pin_memory()
+    k2 = torch.empty((cfg.nq, 10), dtype=torch.uint64).pin_memory()
+    bolt.HostSearch(cfg.n, cfg.j, cfg.m, cfg.nq, 10)(Xh, Qh, dev(C), 0, float(a), dev(b), k1)
+    hs = bolt.HostSearch(cfg.n, cfg.j, cfg.m, cfg.nq, 10, chunks=chunks)
+    for _ in range(2):  # back to back: the second call's copies must wait for the first's compute
+        hs(Xh, Qh, dev(C), 0, float(a), dev(b), k2)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(k2.numpy(), k1.numpy())
+    codes = bolt.encode(dev(X), dev(C))
+    ql = bolt.build_quantized_luts(dev(Q), dev(C), 0, float(a), dev(b))
+    np.testing.assert_array_equal(k1.numpy(), orc.topk(orc.unpack_v1(host(codes), cfg.n, cfg.m), host(ql), 10, 0))
+
+
 # ----------------------------------------------------- c2 at full size (sampled)
 @pytest.mark.slow
 def test_c2_full_size_sampled(bolt, orc):
