@@ -14,7 +14,7 @@ ix = {h: i for i, h in enumerate(hdr)}
 launches = [(r[ix["Kernel Name"]], float(r[ix["Metric Value"]]), r[ix["Metric Unit"]]) for r in rows[start:]
             if len(r) == len(hdr) and r[ix["Metric Name"]] == "gpu__time_duration.sum"]
 scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "msecond": 1.0}
-enc = [i for i, (k, _, _) in enumerate(launches) if "encode_kernel" in k]
+enc = [i for i, (k, _, _) in enumerate(launches) if "encode" in k]
 tot = collections.defaultdict(float)
 for e in enc[-steps:]:  # one step = encode .. the first merge after it
     for k, v, u in launches[e:]:
