@@ -114,6 +114,14 @@ encode_kernel(const float* __restrict__ X, int64_t n, int j, int64_t ldx,
 // 16 floats of the two rows prefetched into registers while the current one
 // is processed (load latency hidden), 256 threads per block.  Same fp32
 // operations in the same order as encode_kernel (bit-identical codes).
+// 32-byte load (sm_100: LDG.E.ENL2.256): one L1TEX request per (row, codebook)
+// slice instead of two 16-byte ones -- the row-strided loads are L1TEX-bound
+__device__ __forceinline__ void ldg256(const float* p, float4& a, float4& b) {
+    asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                 : "l"(p));
+}
+
 constexpr int kEnc2Threads = 256;
 constexpr int kEnc2Rows = 2;
 constexpr int kEnc2RowsPerBlock = kEnc2Threads * kEnc2Rows;  // 512 = 64 groups
@@ -146,9 +154,10 @@ encode_l8_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const floa
     }
     float4 nx[kEnc2Rows][2];
 #pragma unroll
-    for (int r = 0; r < kEnc2Rows; ++r)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) nx[r][h] = valid[r] ? __ldg(xr[r] + h) : make_float4(0, 0, 0, 0);
+    for (int r = 0; r < kEnc2Rows; ++r) {
+        if (valid[r]) ldg256(reinterpret_cast<const float*>(xr[r]), nx[r][0], nx[r][1]);
+        else nx[r][0] = nx[r][1] = make_float4(0, 0, 0, 0);
+    }
     for (int c = 0; c < m; ++c) {
         float xv[kEnc2Rows][L];
 #pragma unroll
@@ -159,8 +168,7 @@ encode_l8_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const floa
         if (c + 1 < m) {
 #pragma unroll
             for (int r = 0; r < kEnc2Rows; ++r)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) nx[r][h] = valid[r] ? __ldg(xr[r] + 2 * (c + 1) + h) : make_float4(0, 0, 0, 0);
+                if (valid[r]) ldg256(reinterpret_cast<const float*>(xr[r] + 2 * (c + 1)), nx[r][0], nx[r][1]);
         }
         float2 d[kEnc2Rows][kK / 2];
 #pragma unroll
@@ -245,7 +253,7 @@ cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const f
     size_t smem = (size_t)j * kK * sizeof(float) + (size_t)kEncGroupsPerBlock * m * sizeof(uint32_t);
     bool vec = (L % 4 == 0) && (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
     int64_t blocks = ceil_div(n, kEncRowsPerBlock);
-    if (vec && L == 8) {
+    if (vec && L == 8 && (ldx % 8) == 0 && (reinterpret_cast<uintptr_t>(X) & 31) == 0) {
         static_assert(kEnc2RowsPerBlock == kEncRowsPerBlock, "same 64-group staging");
         cudaFuncSetAttribute(encode_l8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         encode_l8_kernel<<<(unsigned)blocks, kEnc2Threads, smem, s>>>(X, n, ldx, C, m, codes);

@@ -1,1 +1,1 @@
-for cl in 0 100 200 300 350; do echo "== cluster=$cl"; BOLT_TRACE_CLUSTER=$cl BOLT_LIB=libbolt_x.so BOLT_TC_XMODE=64 TRACE_OUT=gpurun_out/trace_cl$cl.npy timeout 120 python tools/trace_scan.py --variant tc --config c2 | grep -E "cadence|processing|tiles traced"; done
+for i in 1 2; do timeout 120 python tools/prof_scan.py --what encode --reps 10; done
