@@ -88,6 +88,8 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // ---- top-k plan shared by workspace sizing and execution
 struct TopkPlan {
     int variant;     // resolved PRMT / TC
+    int klist;       // TC: keys per partial list (k, or 32 when k > 32)
+    size_t large_off;  // TC, k > 32: byte offset of flags | count | fallback area in ws
     bool small;      // PRMT: the small-batch kernel (scan_small.cu, nq < 64)
     int parts;
     int64_t pre_n;   // TC: rows of the threshold-seeding prefix pass (0 = none)
@@ -96,6 +98,9 @@ struct TopkPlan {
     size_t pre_off;  // byte offset of the prefix pass's partial lists + thresholds in ws
 };
 
+
+constexpr int kTcListMax = 32;      // register list capacity of the tcgen05 epilogue
+constexpr int kFallbackBatch = 48;  // flagged queries per exact fallback batch (small-batch kernel)
 
 // Rows of the prefix sample that seeds the tcgen05 scan's shared thresholds
 // (scan_tc.cu): its exact top-k gives, per query, a value that at least k
@@ -119,12 +124,20 @@ TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     p.parts = v == BOLT_VARIANT_TC ? topk_tc_parts(n, m, nq, k, sms)
               : p.small           ? topk_small_parts(n, m, nq, k, sms)
                                   : topk_prmt_parts(n, m, nq, k, sms);
-    p.ws = p.parts > 1 || p.small ? (size_t)p.parts * nq * k * sizeof(uint64_t) : 0;
+    p.klist = v == BOLT_VARIANT_TC && k > kTcListMax ? kTcListMax : k;
+    p.ws = p.parts > 1 || p.small ? (size_t)p.parts * nq * p.klist * sizeof(uint64_t) : 0;
     // shared per-query thresholds (u32) after the partial lists: PRMT one word,
     // TC 3 nq + 1 (k-th value words + 8 B aligned half-list pairs, scan_tc.cu),
     // small-batch PRMT 33 nq (k-th value word + 32 minima slots, scan_small.cu)
     if (p.ws > 0) p.ws += (size_t)(v == BOLT_VARIANT_TC ? 3 * nq + 1 : p.small ? 33 * nq : nq) * sizeof(uint32_t);
-    if (v == BOLT_VARIANT_TC && p.parts > 1) {
+    if (v == BOLT_VARIANT_TC && k > kTcListMax) {
+        // flags [nq] u32, count, then the exact fallback for flagged queries in
+        // batches of kFallbackBatch: gathered tables, keys, small-batch workspace
+        p.large_off = align256(p.ws);
+        p.ws = p.large_off + align256((size_t)nq * sizeof(uint32_t) + 16) + align256((size_t)kFallbackBatch * m * kK) +
+               align256((size_t)kFallbackBatch * k * sizeof(uint64_t)) +
+               align256(topk_plan(n, m, kFallbackBatch, k, BOLT_VARIANT_PRMT, sms).ws);
+    } else if (v == BOLT_VARIANT_TC && p.parts > 1) {
         p.pre_n = tc_prefix_rows(n);
         if (p.pre_n > 0) {
             p.pre_parts = topk_tc_parts(p.pre_n, m, nq, k, sms);
@@ -373,6 +386,55 @@ bolt_status bolt_topk_ex(const uint32_t* codes, int64_t n, int m, const uint8_t*
         e = launch_prefix_threshold(pre_keys, p.pre_parts, nq, k, metric, 255u * (uint32_t)m, gthr, s);
         if (e != cudaSuccess) return cuda_status(e, "bolt_topk prefix threshold");
         e = launch_topk_tc(a, k, metric, index_base, p.parts, parts_out, d.sms, s, false);
+    } else if (p.variant == BOLT_VARIANT_TC && k > kTcListMax) {
+        // lists of 32 per (query, partition), no shared thresholds; merged into
+        // k keys; a query is exact unless some list's 32nd key lies below the
+        // merged k-th key -- those queries (rare) are redone exactly by the
+        // PRMT kernels.  One host synchronisation (the flag count).
+        a.noshare = 1;
+        e = launch_topk_tc(a, kTcListMax, metric, index_base, p.parts, parts_out, d.sms, s);
+        if (e != cudaSuccess) return cuda_status(e, "bolt_topk scan");
+        char* lp = static_cast<char*>(ws) + p.large_off;
+        uint32_t* flags = reinterpret_cast<uint32_t*>(lp);
+        uint32_t* count = flags + nq;
+        lp += align256((size_t)nq * sizeof(uint32_t) + 16);
+        uint8_t* fq = reinterpret_cast<uint8_t*>(lp); lp += align256((size_t)kFallbackBatch * m * kK);
+        uint64_t* fk = reinterpret_cast<uint64_t*>(lp); lp += align256((size_t)kFallbackBatch * k * sizeof(uint64_t));
+        void* fws = lp;
+        const size_t fws_bytes = p.ws - (size_t)(lp - static_cast<char*>(ws));
+        TRY(cuda_status(launch_merge_lists(parts_out, p.parts, nq, kTcListMax, k, out_keys, flags, count, s),
+                        "bolt_topk merge"));
+        uint32_t hcount = 0;
+        TRY(cuda_status(cudaMemcpyAsync(&hcount, count, sizeof(uint32_t), cudaMemcpyDeviceToHost, s), "count"));
+        TRY(cuda_status(cudaStreamSynchronize(s), "sync"));
+        if (hcount == 0) return BOLT_OK;
+        uint32_t* hflags = static_cast<uint32_t*>(malloc((size_t)nq * sizeof(uint32_t)));
+        if (!hflags) return fail(BOLT_E_CUDA, "host allocation failed");
+        cudaError_t ce = cudaMemcpy(hflags, flags, (size_t)nq * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+        if (ce != cudaSuccess) { free(hflags); return cuda_status(ce, "flags"); }
+        int64_t qs[kFallbackBatch];
+        int nb = 0;
+        bolt_status st = BOLT_OK;
+        for (int64_t q = 0; q <= nq && st == BOLT_OK; ++q) {
+            if (q < nq && hflags[q]) {
+                ce = cudaMemcpyAsync(fq + (size_t)nb * m * kK, qluts + (size_t)q * m * kK, (size_t)m * kK,
+                                     cudaMemcpyDeviceToDevice, s);
+                if (ce != cudaSuccess) { st = cuda_status(ce, "gather"); break; }
+                qs[nb++] = q;
+            }
+            if (nb == kFallbackBatch || (q == nq && nb > 0)) {
+                st = bolt_topk_ex(codes, n, m, fq, nb, k, metric, index_base, fk, fws, fws_bytes, BOLT_VARIANT_PRMT,
+                                  stream);
+                for (int i = 0; i < nb && st == BOLT_OK; ++i) {
+                    ce = cudaMemcpyAsync(out_keys + qs[i] * k, fk + (size_t)i * k, (size_t)k * sizeof(uint64_t),
+                                         cudaMemcpyDeviceToDevice, s);
+                    if (ce != cudaSuccess) st = cuda_status(ce, "scatter");
+                }
+                nb = 0;
+            }
+        }
+        free(hflags);
+        return st;
     } else if (p.small) {
         if (p.parts == 1) {  // the kernel needs its threshold words: keep them in a 1-list workspace
             e = launch_topk_small(a, k, metric, index_base, 1, static_cast<uint64_t*>(ws), s);

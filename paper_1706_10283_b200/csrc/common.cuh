@@ -86,6 +86,7 @@ struct ScanArgs {
     int m;
     const uint8_t* qluts;
     int64_t nq;
+    int noshare = 0;      // tcgen05 top-k: no shared thresholds (lists shorter than the final k)
 };
 
 }  // namespace bolt
@@ -127,6 +128,9 @@ int topk_small_supported(int64_t n, int m, int64_t nq, int k);
 int topk_small_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
 cudaError_t launch_topk_small(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
                               uint64_t* part_keys, cudaStream_t s);
+// merge of lk-key lists into k keys + exactness flags (large-k tcgen05 top-k)
+cudaError_t launch_merge_lists(const uint64_t* keys, int w, int64_t nq, int lk, int k, uint64_t* out,
+                               uint32_t* flags, uint32_t* count, cudaStream_t s);
 // merge of many lists (k <= 32): bound by the k-th smallest head, then select
 cudaError_t launch_merge_many(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out, cudaStream_t s);
 cudaError_t launch_prefix_threshold(const uint64_t* keys, int w, int64_t nq, int k, int metric, uint32_t kvmax,

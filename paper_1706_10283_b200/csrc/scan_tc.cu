@@ -508,9 +508,14 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
         uint32_t* gq = gthr_inv + (qvalid ? q0 + q : 0);
         uint32_t thr = kNotFull;
         uint32_t* gh = gthr_inv + ((a.nq + 1) & ~int64_t(1)) + 2 * (qvalid ? q0 + q : 0);  // 8 B aligned
-        uint32_t g_next, gh0, gh1;  // inverted shared thresholds (0 = none yet), fetched a tile ahead
-        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g_next) : "l"(gq));
-        asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gh0), "=r"(gh1) : "l"(gh));
+        // a.noshare (lists of 32 for a larger final k): a list's k-th value bounds only
+        // the global 32nd best, so nothing is shared
+        const bool share = a.noshare == 0;
+        uint32_t g_next = 0, gh0 = 0, gh1 = 0;  // inverted shared thresholds (0 = none yet), fetched a tile ahead
+        if (share) {
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g_next) : "l"(gq));
+            asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gh0), "=r"(gh1) : "l"(gh));
+        }
         const uint32_t tlane = (uint32_t)(quad * 32) << 16;
         for (int tile = 0; tile < ntiles; ++tile) {
             const int d = tile & 1;
@@ -625,8 +630,10 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             thr = min(min(own, 0xFFFFu - g_next + 1u), 0xFFFFu - min(gh0, gh1) + 1u);
             if (tile >= 1 && thr > 0xFFFFu) BOLT_PROF_WARP(17, 1);  // lanes without a threshold after tile 0
             if (tile == 1) BOLT_PROF_ADD(18, thr);
-            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g_next) : "l"(gq));
-            asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gh0), "=r"(gh1) : "l"(gh));
+            if (share) {
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g_next) : "l"(gq));
+                asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gh0), "=r"(gh1) : "l"(gh));
+            }
             const int tbl = tile * C::N;  // local index of the tile's first vector
             const int nvalid = (int)min64(C::N, vend - vbeg - tbl);
             // packed u16x2 tree over the warp's 128 columns; the four chunk
@@ -691,11 +698,11 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             __syncwarp();  // reconverge before the next tile's .aligned tcgen05.ld
             if (lane == 0) BOLT_PROF_ADD(8, BOLT_CLOCK() - tp0);  // processing cycles (all warps)
             if (lane == 0) BOLT_TRACE(tile, 27 + warp);
-            if (own < published && qvalid) {
+            if (own < published && qvalid && share) {
                 published = own;
                 asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gq), "r"(0xFFFFu - own) : "memory");
             }
-            if (changed && qvalid) {
+            if (changed && qvalid && share) {
                 changed = false;
                 const uint32_t own_h = list.value_at(hpos, C::IDX_BITS);
                 if (own_h < published_h) {  // published_h = 0 for k == 1 (the half bound is own)
@@ -893,7 +900,8 @@ cudaError_t launch_scan_tc(const ScanArgs& a, uint16_t* out16, float* out32, int
 
 int topk_tc_supported(int64_t n, int m, int64_t nq, int k) {
     (void)nq;
-    return n >= 1 && k >= 1 && k <= tc::kMaxTopk && (m == 8 || m == 16 || m == 32);
+    // k <= 32: register lists of k; 32 < k <= 128: lists of 32 + exactness check (api.cu)
+    return n >= 1 && k >= 1 && k <= kMaxK && (m == 8 || m == 16 || m == 32);
 }
 
 // One CTA pair per two SMs; units = 256-query tiles x row partitions, the

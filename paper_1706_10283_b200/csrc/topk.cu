@@ -15,8 +15,9 @@ constexpr int kMergeThreads = 256;
 // lists (head keys and read positions in shared memory).  Each round the
 // block finds the smallest head (ties impossible: keys are unique except
 // the UINT64_MAX padding), emits it and advances that list.
+// lists of lk keys ([w][nq][lk]) -> k outputs per query
 __global__ void __launch_bounds__(kMergeThreads)
-merge_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int k, uint64_t* __restrict__ out) {
+merge_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int lk, int k, uint64_t* __restrict__ out) {
     extern __shared__ uint64_t mhead[];
     int* mpos = reinterpret_cast<int*>(mhead + w);
     __shared__ uint64_t wkey[kMergeThreads / 32];
@@ -25,7 +26,7 @@ merge_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int k, uint64
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
     for (int p = threadIdx.x; p < w; p += blockDim.x) {
-        mhead[p] = keys[((int64_t)p * nq + q) * k];
+        mhead[p] = keys[((int64_t)p * nq + q) * lk];
         mpos[p] = 0;
     }
     __syncthreads();
@@ -53,7 +54,7 @@ merge_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int k, uint64
             out[q * k + r] = best;
             if (bi >= 0 && best != ~0ull) {
                 const int np = ++mpos[bi];
-                mhead[bi] = np < k ? keys[((int64_t)bi * nq + q) * k + np] : ~0ull;
+                mhead[bi] = np < lk ? keys[((int64_t)bi * nq + q) * lk + np] : ~0ull;
             }
         }
         __syncthreads();
@@ -203,7 +204,35 @@ cudaError_t launch_merge(const uint64_t* keys, int w, int64_t nq, int k, uint64_
     const size_t smem = (size_t)w * (sizeof(uint64_t) + sizeof(int));
     const int threads = w >= kMergeThreads ? kMergeThreads : (int)(((w + 31) / 32) * 32);
     cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    merge_kernel<<<(unsigned)nq, threads, smem, s>>>(keys, w, nq, k, out);
+    merge_kernel<<<(unsigned)nq, threads, smem, s>>>(keys, w, nq, k, k, out);
+    return cudaGetLastError();
+}
+
+// Large-k tcgen05 top-k (32 < k <= 128): the lists hold 32 keys; merge them
+// into k and flag the queries where a list's 32nd key is below the merged k-th
+// key (that list may have dropped keys of the top-k): flags[q] = 1, count++.
+__global__ void verify_lists_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int lk,
+                                    const uint64_t* __restrict__ out, int k, uint32_t* __restrict__ flags,
+                                    uint32_t* __restrict__ count) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const uint64_t kth = out[q * k + k - 1];
+    uint32_t f = 0;
+    for (int p = 0; p < w && !f; ++p) f = keys[((int64_t)p * nq + q) * lk + lk - 1] < kth;
+    flags[q] = f;
+    if (f) atomicAdd(count, 1u);
+}
+
+cudaError_t launch_merge_lists(const uint64_t* keys, int w, int64_t nq, int lk, int k, uint64_t* out,
+                               uint32_t* flags, uint32_t* count, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    const size_t smem = (size_t)w * (sizeof(uint64_t) + sizeof(int));
+    const int threads = w >= kMergeThreads ? kMergeThreads : (int)(((w + 31) / 32) * 32);
+    cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    merge_kernel<<<(unsigned)nq, threads, smem, s>>>(keys, w, nq, lk, k, out);
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+    verify_lists_kernel<<<(unsigned)ceil_div(nq, 128), 128, 0, s>>>(keys, w, nq, lk, out, k, flags, count);
     return cudaGetLastError();
 }
 

@@ -261,6 +261,29 @@ def test_topk_tc_bitexact(bolt, orc, metric, n, m, nq, k, hi, base):
     np.testing.assert_array_equal(got, ref)
 
 
+# 32 < k <= 128 on the tensor cores: lists of 32 merged, verified, and the
+# flagged queries redone exactly (the constant-table and few-partition cases
+# force the fallback; the large random case mostly does not)
+TC_LARGE_K = [(3000, 16, 40, 100, 256), (70_000, 16, 30, 64, 256), (5000, 8, 33, 128, 4), (200_000, 32, 25, 100, 256)]
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+@pytest.mark.parametrize("n,m,nq,k,hi", TC_LARGE_K)
+def test_topk_tc_large_k(bolt, orc, metric, n, m, nq, k, hi):
+    flat = G.random_codes(n, m, n + k)
+    ql = G.random_qluts(nq, m, nq + k, hi=hi)
+    got = host(bolt.topk(pack_on_gpu(bolt, flat), n, dev(ql), k, metric, index_base=7, variant=bolt.VARIANT_TC))
+    np.testing.assert_array_equal(got, orc.topk(flat, ql, k, metric, index_base=7))
+
+
+def test_topk_tc_large_k_all_ties(bolt, orc):
+    n, m, nq, k = 20_000, 16, 26, 100
+    flat = G.random_codes(n, m, 3)
+    ql = np.full((nq, m, 16), 9, np.uint8)
+    got = host(bolt.topk(pack_on_gpu(bolt, flat), n, dev(ql), k, 0, variant=bolt.VARIANT_TC))
+    np.testing.assert_array_equal(got, orc.topk(flat, ql, k, 0))
+
+
 def test_topk_constant_tables_all_ties(bolt, orc):
     """Every distance equal: the answer is the k lowest indices."""
     n, m, nq, k = 3001, 16, 4, 50
