@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--variant", default="auto", choices=["auto", "prmt", "tc"])
     p.add_argument("--n", type=int, default=0, help="override rows per GPU (debug)")
     p.add_argument("--nq", type=int, default=0, help="override queries (debug)")
+    p.add_argument("--k", type=int, default=0, help="override top-k (debug, c5)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--e2e-chunks", type=int, default=8, help="row blocks of the copy/compute-overlapped host search")
@@ -451,6 +452,7 @@ def roofline(variant, n, m, nq, scan_ms, peaks, peak_src, clocks):
         return {"bound": "tensor", "achieved": round(achieved / 1e12, 2), "peak": round(peak / 1e12, 2),
                 "unit": "TOP/s", "frac": round(achieved / peak, 4), "traffic": profile_traffic("tc"),
                 "peak_source": f"int8 dense = 2 x {peak_src} bf16 ({peaks['bf16_tflops']} TFLOP/s)",
+                "nominal_int8_frac": round(achieved / 4.5e15, 4),  # context: B200 dense int8 4.5 POP/s
                 "kernel": "bolt_topk (tcgen05 scan + top-k)", "kernel_ms": round(scan_ms, 4)}
     ops = 2.0 * m * dists
     peak = 148 * 128 * sm_mhz * 1e6
@@ -461,6 +463,210 @@ def roofline(variant, n, m, nq, scan_ms, peaks, peak_src, clocks):
             "kernel": "bolt_topk (PRMT scan + fused top-k)", "kernel_ms": round(scan_ms, 4),
             "hbm_view": {"algorithmic_bytes": n * m // 2 + nq * m * 16 + nq * 10 * 8,
                          "gbs": round((n * m // 2 + nq * m * 16) / t / 1e9, 1)}}
+
+
+# ------------------------------------------------------------------- c5
+def c2_model(bolt, dev):
+    """c2's codebooks and LUT quantizer, fitted on the GPU (offline, untimed);
+    c5 and the sweep reuse them (SURVEY 8(d) c5 recipe)."""
+    import torch
+    cfg2 = G.CONFIGS["c2"]
+    train = G.training(cfg2)
+    return bolt.BoltModel.fit(torch.from_numpy(train).to(dev), cfg2.m,
+                              torch.from_numpy(G.kmeans_init_all(cfg2, len(train))).to(dev),
+                              torch.from_numpy(G.calibration(cfg2, train)).to(dev), cfg2.metrics[0],
+                              iters=cfg2.kmeans_iters)
+
+
+def c5_codes(bolt, model, r0, n, dev, chunk=1 << 20):
+    """Rows [r0, r0 + n) of c5's database: generated on the GPU
+    (synth/gen_gpu.cu, Philox keyed by global row) in 1M-row chunks and encoded
+    at once, so the 51 GB fp32 database never exists whole."""
+    import torch
+    from synth import gpu as synth_gpu
+    m = model.m
+    mu = torch.from_numpy(G.c5_means()).to(dev)
+    codes = torch.empty(max(bolt.codes_words(n, m), 1), dtype=torch.uint32, device=dev)
+    xbuf = torch.empty((chunk, 128), dtype=torch.float32, device=dev)
+    for c0 in range(0, n, chunk):
+        rows = min(chunk, n - c0)
+        synth_gpu.c5_rows(r0 + c0, rows, mu, xbuf[:rows])
+        w0 = c0 // 8 * m
+        bolt.encode(xbuf[:rows], model.C, out=codes[w0:w0 + bolt.codes_words(rows, m)])
+    del xbuf
+    torch.cuda.synchronize()
+    return codes
+
+
+def c5_cpu_baseline(codes, n, m, qlh, k, metric, nq, budget_s=20.0):
+    """The oracle's scan + top-k (O12) over the full GPU code set for sampled
+    queries, extrapolated to all queries ('c5: sampled queries
+    over the full 100M codes, extrapolated')."""
+    from oracle import oracle
+    t0 = time.perf_counter()
+    flat = oracle.unpack_v1(codes, n, m)
+    t_unpack = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.topk(flat, qlh[:1], k, metric)
+    t1 = time.perf_counter() - t0
+    qs = int(max(1, min(len(qlh) - 1, (budget_s - t1) / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    if qs > 1:
+        oracle.topk(flat, qlh[1:1 + qs], k, metric)
+    t_s = (time.perf_counter() - t0 + t1) / (qs + 1)
+    desc = (f"oracle scan + top-{k} of {qs + 1} sampled queries over all {n} codes ({t_s:.2f} s per query; "
+            f"unpacking the codes took {t_unpack:.1f} s, not counted), extrapolated x{nq / (qs + 1):.0f} to {nq} "
+            "queries; tables and encoding not counted (extrapolated)")
+    return n / t_s / 1e9, oracle.num_threads(), desc
+
+
+def run_c5(args):
+    """BASELINE c5: N = 1e8 rows (c2 mixture, generated + encoded on device,
+    row-sharded over the ranks: contiguous ranges of ceil(N/W/8)*8 rows),
+    Q = 65,536, squared L2, top-100.  One step = fused fp64 LUT build/quantize
+    of all queries (every rank, redundantly) + scan/top-k of the local shard
+    (tcgen05 lists of 32, merged + verified) [+ NCCL all-gather of [Q][100]
+    keys + merge for W > 1].  Encoding is setup."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1706_10283_b200 as bolt
+    from paper_1706_10283_b200.dist import gather_keys
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = G.CONFIGS["c5"]
+    n_total = args.n or cfg.n
+    nq, k, metric, m = args.nq or cfg.nq, args.k or cfg.k, cfg.metrics[0], cfg.m
+    shard = -(-n_total // world // 8) * 8 if world > 1 else n_total
+    r0 = rank * shard
+    n = max(0, min(shard, n_total - r0))
+    model = c2_model(bolt, dev)
+    t0 = time.perf_counter()
+    codes = c5_codes(bolt, model, r0, n, dev)
+    setup_s = time.perf_counter() - t0
+    Q = G.queries(cfg, nq)
+    Qd = torch.from_numpy(Q).to(dev)
+    ql = torch.empty((nq, m, 16), dtype=torch.uint8, device=dev)
+    keys = torch.empty((nq, k), dtype=torch.uint64, device=dev)
+    ws = torch.empty(max(bolt.topk_workspace_bytes(n, m, nq, k), 8), dtype=torch.uint8, device=dev)
+    final = torch.empty((nq, k), dtype=torch.uint64, device=dev) if world > 1 else keys
+
+    def scan_op():
+        bolt.topk(codes, n, ql, k, metric, index_base=r0, out=keys, workspace=ws)
+
+    def step():
+        bolt.build_quantized_luts(Qd, model.C, metric, model.a, model.b, out=ql)
+        scan_op()
+        if world > 1:
+            bolt.topk_merge(gather_keys(keys), out=final)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
+                       int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local]))
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = []
+    with clk:
+        t_start.record(stream)
+        for _ in range(args.steps):
+            step()
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        for _ in range(max(1, min(args.steps, 3))):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            scan_op()
+            e1.record(stream)
+            ev.append((e0, e1))
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end)
+    scan_ms = sum(a.elapsed_time(b) for a, b in ev) / len(ev)
+    if world > 1:
+        t = torch.tensor([ms, scan_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, scan_ms = float(t[0]), float(t[1])
+    ms_step = ms / args.steps
+    value = n_total * nq / (ms_step * 1e-3) / 1e9
+
+    # e2e through the public API: queries from pinned host memory in, keys out
+    Qh = torch.from_numpy(Q).pin_memory()
+    kh = torch.empty((nq, k), dtype=torch.uint64).pin_memory()
+
+    def e2e_step():
+        Qd.copy_(Qh, non_blocking=True)
+        step()
+        kh.copy_(final, non_blocking=True)
+
+    e2e = None
+    if args.e2e_steps > 0:
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        a0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a0.elapsed_time(a1) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t[0])
+        e2e = {"value": round(n_total * nq / (e_ms * 1e-3) / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": int(Q.nbytes), "d2h_bytes_per_step": int(nq * k * 8),
+               "ms_per_step": round(e_ms, 3),
+               "api": "bolt.build_quantized_luts / topk [/ all-gather + topk_merge] (pinned host Q in, keys out); "
+                      "the database is device-resident (generated + encoded on the GPU)"}
+
+    peaks, peak_src = measured_peaks()
+    variant, parts = bolt.topk_plan(n, m, nq, k)
+    # a ~1 s kernel: the sustained (power-capped) tensor peak applies if the
+    # clocks show the cap; at full clocks with no throttle reason, the burst one
+    ck = clk.summary()
+    capped = "sw_power_cap" in ck.get("reasons", []) or (ck.get("sm_mhz") or 0) < 0.9 * (ck.get("sm_max_mhz") or 1)
+    pk = dict(peaks)
+    if capped and "bf16_tflops_sustained" in peaks:
+        pk["bf16_tflops"] = peaks["bf16_tflops_sustained"]
+    roof = roofline(variant, n, m, nq, scan_ms, pk, peak_src + (" sustained" if capped else " burst"), ck)
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic (c5: c2 mixture generated on the GPU by Philox4x32-10, SURVEY 8(d))",
+            "config": {"workload": f"c5: N={n_total} rows total ({n} on rank 0), J=128, M=16, Q={nq}, "
+                                   f"squared L2, top-{k}; step = fp64 LUT build/quantize + scan/top-{k}"
+                                   + (" + NCCL all-gather + merge" if world > 1 else "")
+                                   + "; database generated + encoded once at setup "
+                                   f"({setup_s:.1f} s, untimed)",
+                       "n_per_gpu": n, "nq": nq, "m": m, "j": 128, "k": k, "variant": variant,
+                       "scan_parts": parts, "timing": "eager (the top-100 path synchronises once on its flag count)",
+                       "l2": "codes 800 MB / W > L2 at W <= 4; compute-bound (SURVEY 8(d))",
+                       "parallelism": f"row-sharded dp{world}"},
+            "roofline": roof, "e2e": e2e,
+            "gpu_launches": args.steps * (4 + (2 if world > 1 else 0)),  # LUT, scan, merge, verify [+ gather, merge]
+            "clocks": clk.summary(), "scan_ms": round(scan_ms, 3),
+        }
+        if not args.no_cpu_baseline and world == 1:
+            v, cores, desc = c5_cpu_baseline(codes.cpu().numpy(), n, m, ql[:65].cpu().numpy(), k, metric, nq)
+            out["cpu_baseline"] = {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
+                                   "sample": desc}
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
 
 
 # ------------------------------------------------------------------ sweep
@@ -478,28 +684,13 @@ def run_sweep(args):
     import torch
 
     import paper_1706_10283_b200 as bolt
-    from synth import gpu as synth_gpu
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     cfg2, cfg5 = G.CONFIGS["c2"], G.CONFIGS["c5"]
     n = args.n or cfg5.n
-    train = G.training(cfg2)
-    model = bolt.BoltModel.fit(torch.from_numpy(train).to(dev), cfg2.m,
-                               torch.from_numpy(G.kmeans_init_all(cfg2, len(train))).to(dev),
-                               torch.from_numpy(G.calibration(cfg2, train)).to(dev), cfg2.metrics[0],
-                               iters=cfg2.kmeans_iters)
-    mu = torch.from_numpy(G.c5_means()).to(dev)
-    chunk = 1 << 20
-    codes = torch.empty(bolt.codes_words(n, cfg2.m), dtype=torch.uint32, device=dev)
-    xbuf = torch.empty((chunk, 128), dtype=torch.float32, device=dev)
-    for r0 in range(0, n, chunk):
-        rows = min(chunk, n - r0)
-        synth_gpu.c5_rows(r0, rows, mu, xbuf[:rows])
-        w0 = r0 // 8 * cfg2.m
-        bolt.encode(xbuf[:rows], model.C, out=codes[w0:w0 + bolt.codes_words(rows, cfg2.m)])
-    del xbuf
-    torch.cuda.synchronize()
+    model = c2_model(bolt, dev)
+    codes = c5_codes(bolt, model, 0, n, dev)
     Qall = torch.from_numpy(G.queries(cfg5, max(SWEEP_Q))).to(dev)
     peaks, peak_src = measured_peaks()
     stream = torch.cuda.current_stream(dev)
@@ -581,6 +772,8 @@ if __name__ == "__main__":
     a = parse()
     if a.config == "sweep" and a.impl != "reference":
         run_sweep(a)
+    elif a.config == "c5" and a.impl != "reference":
+        run_c5(a)
     elif a.impl == "reference":
         run_reference(a)
     else:

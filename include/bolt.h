@@ -238,6 +238,7 @@ BOLT_API bolt_status bolt_calibrate(const double* luts, int64_t nq, int m, float
  * Returns the number of counters written. */
 BOLT_API int bolt_debug_counters(uint64_t* out, int n);
 
+
 #ifdef __cplusplus
 }
 #endif

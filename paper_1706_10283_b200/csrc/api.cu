@@ -92,27 +92,12 @@ struct TopkPlan {
     size_t large_off;  // TC, k > 32: byte offset of flags | count | fallback area in ws
     bool small;      // PRMT: the small-batch kernel (scan_small.cu, nq < 64)
     int parts;
-    int64_t pre_n;   // TC: rows of the threshold-seeding prefix pass (0 = none)
-    int pre_parts;
     size_t ws;
-    size_t pre_off;  // byte offset of the prefix pass's partial lists + thresholds in ws
 };
 
 
 constexpr int kTcListMax = 32;      // register list capacity of the tcgen05 epilogue
 constexpr int kFallbackBatch = 48;  // flagged queries per exact fallback batch (small-batch kernel)
-
-// Rows of the prefix sample that seeds the tcgen05 scan's shared thresholds
-// (scan_tc.cu): its exact top-k gives, per query, a value that at least k
-// database rows reach, so the full scan never has to fill its lists from
-// scratch.  Used when the database is >= 32x the sample.
-int64_t tc_prefix_rows(int64_t n) {
-    int64_t rows = 0;  // off: measured no net gain on c2 (profiles/r1); kept for sweeps
-#ifdef BOLT_XMODE
-    if (const char* e = getenv("BOLT_TC_PREFIX")) rows = atoll(e);  // diagnostic sweeps (tools/)
-#endif
-    return rows > 0 && n >= 32 * rows ? rows : 0;
-}
 
 TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     TopkPlan p{};
@@ -129,7 +114,9 @@ TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     // shared per-query thresholds (u32) after the partial lists: PRMT one word,
     // TC 3 nq + 1 (k-th value words + 8 B aligned half-list pairs, scan_tc.cu),
     // small-batch PRMT 33 nq (k-th value word + 32 minima slots, scan_small.cu)
-    if (p.ws > 0) p.ws += (size_t)(v == BOLT_VARIANT_TC ? 3 * nq + 1 : p.small ? 33 * nq : nq) * sizeof(uint32_t);
+    if (p.ws > 0)
+        p.ws += (size_t)(v == BOLT_VARIANT_TC ? (k > kTcListMax ? 4 * nq : 3 * nq + 1) : p.small ? 33 * nq : nq) *
+                sizeof(uint32_t);
     if (v == BOLT_VARIANT_TC && k > kTcListMax) {
         // flags [nq] u32, count, then the exact fallback for flagged queries in
         // batches of kFallbackBatch: gathered tables, keys, small-batch workspace
@@ -137,14 +124,6 @@ TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
         p.ws = p.large_off + align256((size_t)nq * sizeof(uint32_t) + 16) + align256((size_t)kFallbackBatch * m * kK) +
                align256((size_t)kFallbackBatch * k * sizeof(uint64_t)) +
                align256(topk_plan(n, m, kFallbackBatch, k, BOLT_VARIANT_PRMT, sms).ws);
-    } else if (v == BOLT_VARIANT_TC && p.parts > 1) {
-        p.pre_n = tc_prefix_rows(n);
-        if (p.pre_n > 0) {
-            p.pre_parts = topk_tc_parts(p.pre_n, m, nq, k, sms);
-            if (p.pre_parts > 32) p.pre_parts = 32;
-            p.pre_off = align256(p.ws);
-            p.ws = p.pre_off + (size_t)p.pre_parts * nq * k * sizeof(uint64_t) + (size_t)(3 * nq + 1) * sizeof(uint32_t);
-        }
     }
     return p;
 }
@@ -376,22 +355,12 @@ bolt_status bolt_topk_ex(const uint32_t* codes, int64_t n, int m, const uint8_t*
     ScanArgs a{codes, n, ceil_div(n, 8), m, qluts, nq};
     uint64_t* parts_out = p.parts > 1 ? static_cast<uint64_t*>(ws) : out_keys;
     cudaError_t e = cudaSuccess;
-    if (p.variant == BOLT_VARIANT_TC && p.pre_n > 0) {
-        // threshold seed: exact top-k of the first pre_n rows -> shared thresholds of the full scan
-        uint64_t* pre_keys = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(ws) + p.pre_off);
-        ScanArgs pa{codes, p.pre_n, ceil_div(p.pre_n, 8), m, qluts, nq};
-        e = launch_topk_tc(pa, k, metric, 0, p.pre_parts, pre_keys, d.sms, s, true);
-        if (e != cudaSuccess) return cuda_status(e, "bolt_topk prefix scan");
-        uint32_t* gthr = reinterpret_cast<uint32_t*>(parts_out + (size_t)p.parts * nq * k);
-        e = launch_prefix_threshold(pre_keys, p.pre_parts, nq, k, metric, 255u * (uint32_t)m, gthr, s);
-        if (e != cudaSuccess) return cuda_status(e, "bolt_topk prefix threshold");
-        e = launch_topk_tc(a, k, metric, index_base, p.parts, parts_out, d.sms, s, false);
-    } else if (p.variant == BOLT_VARIANT_TC && k > kTcListMax) {
+    if (p.variant == BOLT_VARIANT_TC && k > kTcListMax) {
         // lists of 32 per (query, partition), no shared thresholds; merged into
         // k keys; a query is exact unless some list's 32nd key lies below the
         // merged k-th key -- those queries (rare) are redone exactly by the
         // PRMT kernels.  One host synchronisation (the flag count).
-        a.noshare = 1;
+        a.noshare = (k + kTcListMax - 1) / kTcListMax;  // group-shared thresholds (scan_tc.cu)
         e = launch_topk_tc(a, kTcListMax, metric, index_base, p.parts, parts_out, d.sms, s);
         if (e != cudaSuccess) return cuda_status(e, "bolt_topk scan");
         char* lp = static_cast<char*>(ws) + p.large_off;
@@ -449,7 +418,7 @@ bolt_status bolt_topk_ex(const uint32_t* codes, int64_t n, int m, const uint8_t*
     }
     if (e != cudaSuccess) return cuda_status(e, "bolt_topk scan");
     if (p.small && p.parts > 64)
-        return cuda_status(launch_merge_many(parts_out, p.parts, nq, k, out_keys, s), "bolt_topk merge");
+        return cuda_status(launch_merge_many(parts_out, p.parts, nq, k, k, out_keys, s), "bolt_topk merge");
     if (p.parts > 1) return cuda_status(launch_merge(parts_out, p.parts, nq, k, out_keys, s), "bolt_topk merge");
     return BOLT_OK;
 }

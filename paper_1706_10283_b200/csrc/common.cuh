@@ -119,10 +119,9 @@ int scan_tc_supported(int64_t n, int m, int64_t nq);
 cudaError_t launch_scan_tc(const ScanArgs& a, uint16_t* out16, float* out32, int64_t ldo, float inv_a, float b_sum,
                            int sms, cudaStream_t s);
 int topk_tc_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
-// part_keys: parts*nq*k keys followed by nq u32 shared thresholds (zeroed
-// by the launch when init_thresholds, else seeded by the caller)
+// part_keys: parts*nq*k keys followed by the shared threshold words (zeroed by the launch)
 cudaError_t launch_topk_tc(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
-                           uint64_t* part_keys, int sms, cudaStream_t s, bool init_thresholds = true);
+                           uint64_t* part_keys, int sms, cudaStream_t s);
 // small query batches (scan_small.cu): one partial list per warp + shared thresholds
 int topk_small_supported(int64_t n, int m, int64_t nq, int k);
 int topk_small_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
@@ -132,9 +131,8 @@ cudaError_t launch_topk_small(const ScanArgs& a, int k, int metric, int64_t inde
 cudaError_t launch_merge_lists(const uint64_t* keys, int w, int64_t nq, int lk, int k, uint64_t* out,
                                uint32_t* flags, uint32_t* count, cudaStream_t s);
 // merge of many lists (k <= 32): bound by the k-th smallest head, then select
-cudaError_t launch_merge_many(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out, cudaStream_t s);
-cudaError_t launch_prefix_threshold(const uint64_t* keys, int w, int64_t nq, int k, int metric, uint32_t kvmax,
-                                    uint32_t* gthr, cudaStream_t s);
+cudaError_t launch_merge_many(const uint64_t* keys, int w, int64_t nq, int lk, int k, uint64_t* out,
+                              cudaStream_t s);
 constexpr int kMaxParts = 16384;  // merge limit (shared memory of the tournament merge)
 
 int tc_debug_counters(uint64_t* out, int n);  // scan_tc.cu (BOLT_PROFILE builds)

@@ -341,7 +341,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sm
                  : "memory");
 }
 
-template <int M, bool kDot, int KMAX, int kOut = 0>
+template <int M, bool kDot, int KMAX, int kOut = 0, bool kGroup = false>
 __global__ void __launch_bounds__(kThreads, 1)
 topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, uint64_t* __restrict__ part_keys,
                uint32_t* __restrict__ gthr_inv, int xmode, FullOut fo, const __grid_constant__ CUtensorMap omap) {
@@ -508,10 +508,18 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
         uint32_t* gq = gthr_inv + (qvalid ? q0 + q : 0);
         uint32_t thr = kNotFull;
         uint32_t* gh = gthr_inv + ((a.nq + 1) & ~int64_t(1)) + 2 * (qvalid ? q0 + q : 0);  // 8 B aligned
-        // a.noshare (lists of 32 for a larger final k): a list's k-th value bounds only
-        // the global 32nd best, so nothing is shared
-        const bool share = a.noshare == 0;
+        // kGroup (lists of 32 for a final k <= 32 G, G = a.noshare): a list's
+        // 32nd value bounds only 32 values, so the lists of a query are dealt
+        // into G groups (list id mod G) and each group keeps the minimum of its
+        // lists' 32nd values (inverted word gthr_inv[4q + g]); the G group minima
+        // come from G distinct lists, so >= 32 G >= k values lie at or below
+        // their maximum, which bounds the k-th best.
+        constexpr bool share = !kGroup;
+        const int ngrp = kGroup ? a.noshare : 0;  // compile-time 0 outside the large-k instantiations
+        uint32_t* gg = gthr_inv + 4 * (qvalid ? q0 + q : 0);
+        const int grp = kGroup ? (2 * part + half) % ngrp : 0;
         uint32_t g_next = 0, gh0 = 0, gh1 = 0;  // inverted shared thresholds (0 = none yet), fetched a tile ahead
+        uint32_t gs[4] = {0u, 0u, 0u, 0u};      // group words (kGroup)
         if (share) {
             asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g_next) : "l"(gq));
             asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gh0), "=r"(gh1) : "l"(gh));
@@ -627,6 +635,15 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                 continue;
             }
             // shared threshold: use the value fetched one tile ago, prefetch the next
+            if constexpr (kGroup) {
+                // bound = max over the G groups = 0xFFFF - min of the inverted words
+                uint32_t gmin = gs[0];
+#pragma unroll
+                for (int g = 1; g < 4; ++g) gmin = g < ngrp ? min(gmin, gs[g]) : gmin;
+                g_next = gmin;
+                asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gs[0]), "=r"(gs[1]) : "l"(gg));
+                asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gs[2]), "=r"(gs[3]) : "l"(gg + 2));
+            }
             thr = min(min(own, 0xFFFFu - g_next + 1u), 0xFFFFu - min(gh0, gh1) + 1u);
             if (tile >= 1 && thr > 0xFFFFu) BOLT_PROF_WARP(17, 1);  // lanes without a threshold after tile 0
             if (tile == 1) BOLT_PROF_ADD(18, thr);
@@ -698,9 +715,10 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             __syncwarp();  // reconverge before the next tile's .aligned tcgen05.ld
             if (lane == 0) BOLT_PROF_ADD(8, BOLT_CLOCK() - tp0);  // processing cycles (all warps)
             if (lane == 0) BOLT_TRACE(tile, 27 + warp);
-            if (own < published && qvalid && share) {
+            if (own < published && qvalid) {
                 published = own;
-                asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gq), "r"(0xFFFFu - own) : "memory");
+                asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(kGroup ? gg + grp : gq), "r"(0xFFFFu - own)
+                             : "memory");
             }
             if (changed && qvalid && share) {
                 changed = false;
@@ -778,16 +796,16 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
     }
 }
 
-template <int M, bool kDot, int KMAX, int kOut = 0>
+template <int M, bool kDot, int KMAX, int kOut = 0, bool kGroup = false>
 cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, uint64_t* part_keys,
-                      uint32_t* gthr, cudaStream_t s, bool init_thr, FullOut fo = FullOut{},
+                      uint32_t* gthr, cudaStream_t s, FullOut fo = FullOut{},
                       const CUtensorMap& omap = CUtensorMap{}) {
     using C = Cfg<M, (kOut != 0)>;
     const int tiles_q = (int)ceil_div(a.nq, 2 * kQM);
     // full output with TMA stores: partitions of whole 256-vector tiles, so that
     // a tile's 256 rows never reach into the next partition
     const int64_t vpp = fo.tma ? ceil_div(ceil_div(a.n, rparts), C::N) * C::N : ceil_div(ceil_div(a.n, rparts), 8) * 8;
-    auto kern = topk_tc_kernel<M, kDot, KMAX, kOut>;
+    auto kern = topk_tc_kernel<M, kDot, KMAX, kOut, kGroup>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(2 * tiles_q * rparts));
@@ -806,10 +824,12 @@ cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, 
     if (const char* x = getenv("BOLT_TC_XMODE")) xmode = atoi(x);
 #endif
     // shared thresholds: [nq] k-th-value words, then (8 B aligned) [nq][2] half-list words
-    if (kOut == 0 && !(xmode & 16)) {  // diagnostic 16: keep caller-prefilled shared thresholds
+    if (kOut == 0 && kGroup) {  // large k: [nq][4] group words instead
+        cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)a.nq * 4 * sizeof(uint32_t), s);
+        if (e != cudaSuccess) return e;
+    } else if (kOut == 0 && !(xmode & 16)) {  // diagnostic 16: keep caller-prefilled shared thresholds
         const int64_t hoff = (a.nq + 1) & ~int64_t(1);
-        cudaError_t e = init_thr ? cudaMemsetAsync(gthr, 0, (size_t)(hoff + 2 * a.nq) * sizeof(uint32_t), s)
-                                 : cudaMemsetAsync(gthr + hoff, 0, (size_t)a.nq * 2 * sizeof(uint32_t), s);
+        cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)(hoff + 2 * a.nq) * sizeof(uint32_t), s);
         if (e != cudaSuccess) return e;
     }
     return cudaLaunchKernelEx(&cfg, kern, a, k, index_base, vpp, tiles_q, part_keys, gthr, xmode, fo, omap);
@@ -819,8 +839,8 @@ cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, 
 template <int M>
 cudaError_t launch_full_m(const ScanArgs& a, int rparts, FullOut fo, const CUtensorMap& omap, bool f32,
                           cudaStream_t s) {
-    return f32 ? launch_mk<M, false, 4, 2>(a, 1, 0, rparts, nullptr, nullptr, s, false, fo, omap)
-               : launch_mk<M, false, 4, 1>(a, 1, 0, rparts, nullptr, nullptr, s, false, fo, omap);
+    return f32 ? launch_mk<M, false, 4, 2>(a, 1, 0, rparts, nullptr, nullptr, s, fo, omap)
+               : launch_mk<M, false, 4, 1>(a, 1, 0, rparts, nullptr, nullptr, s, fo, omap);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
@@ -841,20 +861,23 @@ inline EncodeTiledFn encode_tiled() {
 
 template <int M>
 cudaError_t launch_m(const ScanArgs& a, int k, int metric, int64_t index_base, int rparts, uint64_t* part_keys,
-                     uint32_t* gthr, cudaStream_t s, bool it) {
+                     uint32_t* gthr, cudaStream_t s) {
     const bool dot = metric == BOLT_DOT;
     // register list capacity: smallest of {4, 12, 16, 32} >= k (bubble cost ~ 2 KMAX)
     if (k <= 4)
-        return dot ? launch_mk<M, true, 4>(a, k, index_base, rparts, part_keys, gthr, s, it)
-                   : launch_mk<M, false, 4>(a, k, index_base, rparts, part_keys, gthr, s, it);
+        return dot ? launch_mk<M, true, 4>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 4>(a, k, index_base, rparts, part_keys, gthr, s);
     if (k <= 12)
-        return dot ? launch_mk<M, true, 12>(a, k, index_base, rparts, part_keys, gthr, s, it)
-                   : launch_mk<M, false, 12>(a, k, index_base, rparts, part_keys, gthr, s, it);
+        return dot ? launch_mk<M, true, 12>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 12>(a, k, index_base, rparts, part_keys, gthr, s);
     if (k <= 16)
-        return dot ? launch_mk<M, true, 16>(a, k, index_base, rparts, part_keys, gthr, s, it)
-                   : launch_mk<M, false, 16>(a, k, index_base, rparts, part_keys, gthr, s, it);
-    return dot ? launch_mk<M, true, 32>(a, k, index_base, rparts, part_keys, gthr, s, it)
-               : launch_mk<M, false, 32>(a, k, index_base, rparts, part_keys, gthr, s, it);
+        return dot ? launch_mk<M, true, 16>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 16>(a, k, index_base, rparts, part_keys, gthr, s);
+    if (a.noshare > 0)  // lists of 32 for k > 32: group-shared thresholds
+        return dot ? launch_mk<M, true, 32, 0, true>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 32, 0, true>(a, k, index_base, rparts, part_keys, gthr, s);
+    return dot ? launch_mk<M, true, 32>(a, k, index_base, rparts, part_keys, gthr, s)
+               : launch_mk<M, false, 32>(a, k, index_base, rparts, part_keys, gthr, s);
 }
 
 }  // namespace tc
@@ -920,14 +943,14 @@ int topk_tc_parts(int64_t n, int m, int64_t nq, int k, int num_sms) {
 
 // part_keys holds parts*nq*k keys followed by nq u32 shared thresholds.
 cudaError_t launch_topk_tc(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
-                           uint64_t* part_keys, int sms, cudaStream_t s, bool init_thresholds) {
+                           uint64_t* part_keys, int sms, cudaStream_t s) {
     (void)sms;
     const int rparts = parts / 2;
     uint32_t* gthr = reinterpret_cast<uint32_t*>(part_keys + (size_t)parts * a.nq * k);
     switch (a.m) {
-        case 8: return tc::launch_m<8>(a, k, metric, index_base, rparts, part_keys, gthr, s, init_thresholds);
-        case 16: return tc::launch_m<16>(a, k, metric, index_base, rparts, part_keys, gthr, s, init_thresholds);
-        case 32: return tc::launch_m<32>(a, k, metric, index_base, rparts, part_keys, gthr, s, init_thresholds);
+        case 8: return tc::launch_m<8>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+        case 16: return tc::launch_m<16>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+        case 32: return tc::launch_m<32>(a, k, metric, index_base, rparts, part_keys, gthr, s);
         default: return cudaErrorInvalidValue;
     }
 }

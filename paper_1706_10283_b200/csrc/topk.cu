@@ -61,81 +61,64 @@ merge_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int lk, int k
     }
 }
 
-// Merge of many partial lists (the small-batch scan: one list per block).
-// The k smallest list heads are k distinct keys, so the k-th smallest head H
-// bounds the k-th key of the union; only keys <= H can be in the result, and
-// they lie in the k lists whose heads are <= H: at most k*k survivors.
-//   1. heads -> shared memory; k rounds of argmin give H (no global loads
-//      inside the rounds)
+// Merge of many partial lists ([w][nq][lk] sorted keys -> k per query), for
+// the small-batch scan (one list per block) and the large-k tcgen05 lists.
+// With r = ceil(k / w) leading keys of every list as candidates, the
+// candidate of rank k-1 is the largest of k distinct keys, so it bounds the
+// k-th key of the union (H); only keys <= H can be in the result.  If w > k
+// (r = 1) they lie in the k lists whose heads are <= H, else w <= k lists
+// hold them all: at most min(w, k) * lk survivors.
+//   1. candidates -> shared memory; H = the candidate of rank k-1 (rank by
+//      counting smaller candidates, all threads, no serial rounds)
 //   2. one coalesced pass over all keys keeps those <= H
-//   3. k rounds of argmin over the survivors
-// Used for k <= kFilteredMaxK (k*k survivors fit in shared memory).
-constexpr int kFilteredMaxK = 32;
-
-// One block per query: all threads load the heads and scan the keys (many
-// independent loads in flight), warp 0 alone runs the k-round selections
-// (no block barrier inside a round).
-__device__ __forceinline__ void warp_argmin(uint64_t& best, int& bi) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        const uint64_t o = __shfl_xor_sync(0xffffffffu, best, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (o < best || (o == best && (unsigned)oi < (unsigned)bi)) { best = o; bi = oi; }
-    }
-}
+//   3. each survivor's rank among the survivors is its output slot
+// Keys are distinct except the UINT64_MAX padding, which never survives.
+constexpr int kMergeManySmem = 200 * 1024;
 
 __global__ void __launch_bounds__(kMergeThreads)
-merge_many_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int k, uint64_t* __restrict__ out) {
-    extern __shared__ uint64_t heads[];  // [w] heads, then [k*k] survivors
-    uint64_t* surv = heads + w;
+merge_many_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int lk, int k, int r,
+                  uint64_t* __restrict__ out) {
+    extern __shared__ uint64_t cand[];  // [w * r] candidates, then the survivors
+    const int nc = w * r;
+    uint64_t* surv = cand + nc;
     __shared__ uint64_t sbound;
     __shared__ int count;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t q = blockIdx.x;
-    for (int p = threadIdx.x; p < w; p += blockDim.x) heads[p] = keys[((int64_t)p * nq + q) * k];
-    if (threadIdx.x == 0) count = 0;
+    for (int e = threadIdx.x; e < nc; e += blockDim.x) {
+        const int p = e / r, t = e - p * r;
+        cand[e] = t < lk ? keys[((int64_t)p * nq + q) * lk + t] : ~0ull;
+    }
+    if (threadIdx.x == 0) { count = 0; sbound = ~0ull; }
     __syncthreads();
-    if (warp == 0) {
-        uint64_t bound = ~0ull;
-        for (int r = 0; r < k; ++r) {
-            uint64_t best = ~0ull;
-            int bi = -1;
-            for (int p = lane; p < w; p += 32)
-                if (heads[p] < best) { best = heads[p]; bi = p; }
-            warp_argmin(best, bi);
-            if (bi < 0 || best == ~0ull) break;  // fewer than k keys in all lists
-            bound = best;
-            if (lane == 0) heads[bi] = ~0ull;
-            __syncwarp();
-        }
-        if (lane == 0) sbound = bound;
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+        const uint64_t c = cand[i];
+        if (c == ~0ull) continue;
+        int below = 0;
+        for (int j = 0; j < nc && below < k; ++j) below += cand[j] < c;
+        if (below == k - 1) sbound = c;  // unique: candidates are distinct
     }
     __syncthreads();
-    const uint64_t bound = sbound;
-    const int64_t total = (int64_t)w * k;
+    const uint64_t bound = sbound;  // UINT64_MAX if fewer than k keys: all keys survive
+    const int64_t total = (int64_t)w * lk;
     for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
-        const int p = (int)(e / k), rr = (int)(e - (int64_t)p * k);
-        const uint64_t key = keys[((int64_t)p * nq + q) * k + rr];
-        if (key <= bound && key != ~0ull) {
-            const int slot = atomicAdd(&count, 1);
-            if (slot < k * k) surv[slot] = key;
-        }
+        const int p = (int)(e / lk), t = (int)(e - (int64_t)p * lk);
+        const uint64_t key = keys[((int64_t)p * nq + q) * lk + t];
+        if (key <= bound && key != ~0ull) surv[atomicAdd(&count, 1)] = key;
     }
     __syncthreads();
-    if (warp != 0) return;
-    const int n = min(count, k * k);
-    for (int r = 0; r < k; ++r) {
-        uint64_t best = ~0ull;
-        int bi = -1;
-        for (int i = lane; i < n; i += 32)
-            if (surv[i] < best) { best = surv[i]; bi = i; }
-        warp_argmin(best, bi);
-        if (lane == 0) {
-            out[q * k + r] = best;
-            if (bi >= 0) surv[bi] = ~0ull;
-        }
-        __syncwarp();
+    const int n = count;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint64_t key = surv[i];
+        int below = 0;
+        for (int j = 0; j < n && below < k; ++j) below += surv[j] < key;
+        if (below < k) out[q * k + below] = key;
     }
+    for (int i = n + threadIdx.x; i < k; i += blockDim.x) out[q * k + i] = ~0ull;
+}
+
+size_t merge_many_smem(int w, int lk, int k) {
+    const int r = (k + w - 1) / w;
+    return ((size_t)w * r + (size_t)(w < k ? w : k) * lk) * sizeof(uint64_t);
 }
 
 __global__ void keys_split_kernel(const uint64_t* __restrict__ keys, int64_t count, int metric,
@@ -154,49 +137,9 @@ __global__ void keys_split_kernel(const uint64_t* __restrict__ keys, int64_t cou
     if (idx) idx[e] = (int64_t)(key & ((1ull << 48) - 1));
 }
 
-// Shared-threshold seed from a prefix sample (scan_tc.cu): per query the k-th
-// smallest key of the union of w sorted partial lists over the sample rows,
-// converted to the tcgen05 epilogue's inverted threshold 0xFFFF - kv'
-// (kv' = acc for L2, 255 M - acc for dot).  Every row of the sample is a row
-// of the database, so at least k keys of the full top-k search have a value
-// <= that one: a valid bound for the full scan (0 = no bound if the sample
-// holds fewer than k keys).
-__global__ void prefix_threshold_kernel(const uint64_t* __restrict__ keys, int w, int64_t nq, int k, int metric,
-                                        uint32_t kvmax, uint32_t* __restrict__ gthr) {
-    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= nq) return;
-    int pos[32];
-    for (int p = 0; p < w; ++p) pos[p] = 0;
-    uint64_t kth = ~0ull;
-    for (int r = 0; r < k; ++r) {
-        uint64_t best = ~0ull;
-        int bi = -1;
-        for (int p = 0; p < w; ++p) {
-            const uint64_t h = pos[p] < k ? keys[((int64_t)p * nq + q) * k + pos[p]] : ~0ull;
-            if (h < best) { best = h; bi = p; }
-        }
-        if (bi < 0) break;
-        ++pos[bi];
-        kth = best;
-    }
-    uint32_t g = 0;
-    if (kth != ~0ull) {
-        const uint32_t v = (uint32_t)(kth >> 48);
-        const uint32_t kvp = metric == BOLT_DOT ? kvmax - (0xFFFFu - v) : v;
-        g = 0xFFFFu - kvp;
-    }
-    gthr[q] = g;
-}
 
 }  // namespace
 
-cudaError_t launch_prefix_threshold(const uint64_t* keys, int w, int64_t nq, int k, int metric, uint32_t kvmax,
-                                    uint32_t* gthr, cudaStream_t s) {
-    if (nq == 0) return cudaSuccess;
-    if (w > 32) return cudaErrorInvalidValue;
-    prefix_threshold_kernel<<<(unsigned)ceil_div(nq, 128), 128, 0, s>>>(keys, w, nq, k, metric, kvmax, gthr);
-    return cudaGetLastError();
-}
 
 cudaError_t launch_merge(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out,
                          cudaStream_t s) {
@@ -226,22 +169,27 @@ __global__ void verify_lists_kernel(const uint64_t* __restrict__ keys, int w, in
 cudaError_t launch_merge_lists(const uint64_t* keys, int w, int64_t nq, int lk, int k, uint64_t* out,
                                uint32_t* flags, uint32_t* count, cudaStream_t s) {
     if (nq == 0) return cudaSuccess;
-    const size_t smem = (size_t)w * (sizeof(uint64_t) + sizeof(int));
-    const int threads = w >= kMergeThreads ? kMergeThreads : (int)(((w + 31) / 32) * 32);
-    cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    merge_kernel<<<(unsigned)nq, threads, smem, s>>>(keys, w, nq, lk, k, out);
-    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint32_t), s);
+    cudaError_t e = launch_merge_many(keys, w, nq, lk, k, out, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(count, 0, sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;
     verify_lists_kernel<<<(unsigned)ceil_div(nq, 128), 128, 0, s>>>(keys, w, nq, lk, out, k, flags, count);
     return cudaGetLastError();
 }
 
-cudaError_t launch_merge_many(const uint64_t* keys, int w, int64_t nq, int k, uint64_t* out, cudaStream_t s) {
+cudaError_t launch_merge_many(const uint64_t* keys, int w, int64_t nq, int lk, int k, uint64_t* out,
+                              cudaStream_t s) {
     if (nq == 0) return cudaSuccess;
-    const size_t smem = (size_t)(w + k * k) * sizeof(uint64_t);
-    if (k > kFilteredMaxK || smem > 200 * 1024) return launch_merge(keys, w, nq, k, out, s);
+    const size_t smem = merge_many_smem(w, lk, k);
+    if (smem > kMergeManySmem) {
+        const size_t tsmem = (size_t)w * (sizeof(uint64_t) + sizeof(int));
+        const int threads = w >= kMergeThreads ? kMergeThreads : (int)(((w + 31) / 32) * 32);
+        cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+        merge_kernel<<<(unsigned)nq, threads, tsmem, s>>>(keys, w, nq, lk, k, out);
+        return cudaGetLastError();
+    }
     cudaFuncSetAttribute(merge_many_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    merge_many_kernel<<<(unsigned)nq, kMergeThreads, smem, s>>>(keys, w, nq, k, out);
+    merge_many_kernel<<<(unsigned)nq, kMergeThreads, smem, s>>>(keys, w, nq, lk, k, (k + w - 1) / w, out);
     return cudaGetLastError();
 }
 

@@ -264,7 +264,10 @@ def test_topk_tc_bitexact(bolt, orc, metric, n, m, nq, k, hi, base):
 # 32 < k <= 128 on the tensor cores: lists of 32 merged, verified, and the
 # flagged queries redone exactly (the constant-table and few-partition cases
 # force the fallback; the large random case mostly does not)
-TC_LARGE_K = [(3000, 16, 40, 100, 256), (70_000, 16, 30, 64, 256), (5000, 8, 33, 128, 4), (200_000, 32, 25, 100, 256)]
+# (n, m, nq, k, table max): 1M rows give 488 lists of 32 per query (more
+# lists than k: the merge's heads bound), the others fewer lists than k
+TC_LARGE_K = [(3000, 16, 40, 100, 256), (70_000, 16, 30, 64, 256), (5000, 8, 33, 128, 4), (200_000, 32, 25, 100, 256),
+              (1_000_000, 16, 24, 100, 256), (1_000_000, 16, 26, 40, 16)]
 
 
 @pytest.mark.parametrize("metric", [0, 1])
@@ -436,6 +439,38 @@ def test_c5_device_rows_sampled(bolt, orc):
         ql = bolt.build_quantized_luts(dev(Q[:nq]), dev(C), 0, float(a), dev(b))
         keys = host(bolt.topk(codes, n, ql, 10, 0, index_base=r0, variant=variant))
         np.testing.assert_array_equal(keys, orc.topk(gcodes, host(ql), 10, 0, index_base=r0))
+
+
+@pytest.mark.slow
+def test_c5_full_size_sampled(bolt, orc):
+    """BASELINE c5 on one GPU in bench.py's launch configuration: the 1e8-row
+    device-generated database encoded in 1M-row chunks, Q = 65,536, top-100
+    (tcgen05 lists of 32 over 382 partitions, merged and verified); the oracle
+    checks 3 sampled queries over the full 800 MB of GPU codes (read with O12)."""
+    import torch
+    from synth import gpu as sg
+    cfg2, cfg5 = G.CONFIGS["c2"], G.CONFIGS["c5"]
+    n, m = cfg5.n, cfg2.m
+    train = G.training(cfg2, 20_000)
+    C = orc.fit(train, m, G.kmeans_init_all(cfg2, len(train)), 3)
+    a, b, _ = orc.fit_quantizer(G.calibration(cfg2, train)[:200], C, 0)
+    Cd, mu = dev(C), dev(G.c5_means())
+    codes = torch.empty(bolt.codes_words(n, m), dtype=torch.uint32, device="cuda")
+    chunk = 1 << 20
+    X = torch.empty((chunk, 128), dtype=torch.float32, device="cuda")
+    for r0 in range(0, n, chunk):
+        rows = min(chunk, n - r0)
+        sg.c5_rows(r0, rows, mu, X[:rows])
+        w0 = r0 // 8 * m
+        bolt.encode(X[:rows], Cd, out=codes[w0:w0 + bolt.codes_words(rows, m)])
+    del X
+    ql = bolt.build_quantized_luts(dev(G.queries(cfg5)), Cd, 0, float(a), dev(b))
+    assert bolt.topk_plan(n, m, cfg5.nq, cfg5.k)[0] == "tc"
+    keys = host(bolt.topk(codes, n, ql, cfg5.k, 0))
+    qs = np.random.default_rng(5).choice(cfg5.nq, 3, replace=False)
+    qlh = host(ql[torch.from_numpy(qs).cuda()])
+    gcodes = orc.unpack_v1(host(codes), n, m)
+    np.testing.assert_array_equal(keys[qs], orc.topk(gcodes, qlh, cfg5.k, 0))
 
 
 # ------------------------------------------------------- offline fit (f1)
