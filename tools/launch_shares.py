@@ -1,6 +1,7 @@
 """Per-kernel share of the bench step from an ncu launch list (gpu__time_duration.sum CSV).
-    python tools/launch_shares.py launches.csv [steps=2] > shares.json
-Each of the last `steps` steps is the run of kernels from an encode to the next merge."""
+    python tools/launch_shares.py launches.csv [steps=2] [start=encode] [end=merge_kernel] > shares.json
+Each of the last `steps` steps is the run of kernels from a `start` kernel to
+the next `end` kernel (c5: start=build_luts end=verify_lists)."""
 import collections
 import csv
 import json
@@ -14,12 +15,14 @@ ix = {h: i for i, h in enumerate(hdr)}
 launches = [(r[ix["Kernel Name"]], float(r[ix["Metric Value"]]), r[ix["Metric Unit"]]) for r in rows[start:]
             if len(r) == len(hdr) and r[ix["Metric Name"]] == "gpu__time_duration.sum"]
 scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "msecond": 1.0}
-enc = [i for i, (k, _, _) in enumerate(launches) if "encode" in k]
+start_k = sys.argv[3] if len(sys.argv) > 3 else "encode"
+end_k = sys.argv[4] if len(sys.argv) > 4 else "merge_kernel"
+enc = [i for i, (k, _, _) in enumerate(launches) if start_k in k]
 tot = collections.defaultdict(float)
 for e in enc[-steps:]:  # one step = encode .. the first merge after it
     for k, v, u in launches[e:]:
         tot[k.split("(")[0]] += v * scale.get(u, 1e-6)
-        if "merge_kernel" in k:
+        if end_k in k:
             break
 step = sum(tot.values()) / steps
 print(json.dumps({"source": sys.argv[1], "steps": steps, "step_ms": round(step, 4),

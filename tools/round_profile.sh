@@ -24,3 +24,8 @@ python tools/prof_scan.py --variant prmt --reps 2 --n 20000000 --nq 1 > gpurun_o
 python tools/prof_scan.py --what encode --reps 2 > gpurun_out/p4.txt 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:encode -s 1 -c 1 -o gpurun_out/enc -f \
   python tools/prof_scan.py --what encode --reps 2 > gpurun_out/ncu_enc.log 2>&1
+python bench.py --config c5 --steps 3 --warmup 3 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
+python bench.py --config c5 --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 0 > gpurun_out/c5_plain.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name regex:"topk|merge|verify|lut" --csv \
+  --log-file gpurun_out/launches_bench_c5.csv \
+  python bench.py --config c5 --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ncu_c5_launch.log 2>&1
