@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--n", type=int, default=0, help="override rows per GPU (debug)")
     p.add_argument("--nq", type=int, default=0, help="override queries (debug)")
     p.add_argument("--k", type=int, default=0, help="override top-k (debug, c5)")
+    p.add_argument("--parallel", default="row", choices=["row", "query"],
+                   help="c5 with N > 1: row-sharded database (all-gather + merge) or replicated database with "
+                        "the queries split over the ranks (gather of disjoint slices, SURVEY 8(f4))")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--e2e-chunks", type=int, default=8, help="row blocks of the copy/compute-overlapped host search")
@@ -543,18 +546,26 @@ def run_c5(args):
     cfg = G.CONFIGS["c5"]
     n_total = args.n or cfg.n
     nq, k, metric, m = args.nq or cfg.nq, args.k or cfg.k, cfg.metrics[0], cfg.m
-    shard = -(-n_total // world // 8) * 8 if world > 1 else n_total
-    r0 = rank * shard
-    n = max(0, min(shard, n_total - r0))
+    qmode = args.parallel == "query" and world > 1
+    from paper_1706_10283_b200.dist import gather_query_slices, query_range
+    if qmode:  # every rank holds the whole database and a slice of the queries
+        r0, n = 0, n_total
+        qa, qb = query_range(nq, world, rank)
+    else:
+        shard = -(-n_total // world // 8) * 8 if world > 1 else n_total
+        r0 = rank * shard
+        n = max(0, min(shard, n_total - r0))
+        qa, qb = 0, nq
     model = c2_model(bolt, dev)
     t0 = time.perf_counter()
     codes = c5_codes(bolt, model, r0, n, dev)
     setup_s = time.perf_counter() - t0
-    Q = G.queries(cfg, nq)
+    Q = G.queries(cfg, nq)[qa:qb]
+    nql = qb - qa
     Qd = torch.from_numpy(Q).to(dev)
-    ql = torch.empty((nq, m, 16), dtype=torch.uint8, device=dev)
-    keys = torch.empty((nq, k), dtype=torch.uint64, device=dev)
-    ws = torch.empty(max(bolt.topk_workspace_bytes(n, m, nq, k), 8), dtype=torch.uint8, device=dev)
+    ql = torch.empty((nql, m, 16), dtype=torch.uint8, device=dev)
+    keys = torch.empty((nql, k), dtype=torch.uint64, device=dev)
+    ws = torch.empty(max(bolt.topk_workspace_bytes(n, m, nql, k), 8), dtype=torch.uint8, device=dev)
     final = torch.empty((nq, k), dtype=torch.uint64, device=dev) if world > 1 else keys
 
     def scan_op():
@@ -563,7 +574,9 @@ def run_c5(args):
     def step():
         bolt.build_quantized_luts(Qd, model.C, metric, model.a, model.b, out=ql)
         scan_op()
-        if world > 1:
+        if qmode:
+            final.copy_(gather_query_slices(keys, nq))
+        elif world > 1:
             bolt.topk_merge(gather_keys(keys), out=final)
 
     for _ in range(args.warmup):
@@ -632,7 +645,7 @@ def run_c5(args):
                       "the database is device-resident (generated + encoded on the GPU)"}
 
     peaks, peak_src = measured_peaks()
-    variant, parts = bolt.topk_plan(n, m, nq, k)
+    variant, parts = bolt.topk_plan(n, m, nql, k)
     # a ~1 s kernel: the sustained (power-capped) tensor peak applies if the
     # clocks show the cap; at full clocks with no throttle reason, the burst one
     ck = clk.summary()
@@ -640,7 +653,7 @@ def run_c5(args):
     pk = dict(peaks)
     if capped and "bf16_tflops_sustained" in peaks:
         pk["bf16_tflops"] = peaks["bf16_tflops_sustained"]
-    roof = roofline(variant, n, m, nq, scan_ms, pk, peak_src + (" sustained" if capped else " burst"), ck)
+    roof = roofline(variant, n, m, nql, scan_ms, pk, peak_src + (" sustained" if capped else " burst"), ck)
     if rank == 0:
         out = {
             "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
@@ -649,19 +662,20 @@ def run_c5(args):
             "dtype": "u8", "data": "synthetic (c5: c2 mixture generated on the GPU by Philox4x32-10, SURVEY 8(d))",
             "config": {"workload": f"c5: N={n_total} rows total ({n} on rank 0), J=128, M=16, Q={nq}, "
                                    f"squared L2, top-{k}; step = fp64 LUT build/quantize + scan/top-{k}"
-                                   + (" + NCCL all-gather + merge" if world > 1 else "")
+                                   + ((" + NCCL all-gather of the query slices (replicated database)" if qmode
+                                       else " + NCCL all-gather + merge") if world > 1 else "")
                                    + "; database generated + encoded once at setup "
                                    f"({setup_s:.1f} s, untimed)",
                        "n_per_gpu": n, "nq": nq, "m": m, "j": 128, "k": k, "variant": variant,
                        "scan_parts": parts, "timing": "eager (the top-100 path synchronises once on its flag count)",
                        "l2": "codes 800 MB / W > L2 at W <= 4; compute-bound (SURVEY 8(d))",
-                       "parallelism": f"row-sharded dp{world}"},
+                       "parallelism": f"{'query' if qmode else 'row'}-sharded dp{world}"},
             "roofline": roof, "e2e": e2e,
             "gpu_launches": args.steps * (4 + (2 if world > 1 else 0)),  # LUT, scan, merge, verify [+ gather, merge]
             "clocks": clk.summary(), "scan_ms": round(scan_ms, 3),
         }
         if not args.no_cpu_baseline and world == 1:
-            v, cores, desc = c5_cpu_baseline(codes.cpu().numpy(), n, m, ql[:65].cpu().numpy(), k, metric, nq)
+            v, cores, desc = c5_cpu_baseline(codes.cpu().numpy(), n, m, ql[:65].cpu().numpy(), k, metric, nql)
             out["cpu_baseline"] = {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
                                    "sample": desc}
         print(json.dumps(out))

@@ -95,6 +95,19 @@ BOLT_API int64_t bolt_codes_words(int64_t n, int m);     /* (host) ceil(n/8)*m, 
 BOLT_API bolt_status bolt_encode(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,
                         uint32_t* codes, bolt_stream_t stream);
 
+/* Streaming encode-on-write (the write path T_h of P:L72-89,
+ * P:L141): encode n_new rows and append them to a live code buffer holding
+ * n_old rows, i.e. afterwards `codes` equals bolt_encode of the n_old + n_new
+ * rows (bit for bit; same fp32 operations).  When n_old % 8 != 0 the first
+ * layout-v1 group is partial: its existing nibbles are kept and the new rows
+ * fill the rest (a read-modify-write of that group's m words).
+ *   X, j, ldx, C, m as for bolt_encode (X = the n_new new rows)
+ *   codes in/out: capacity bolt_codes_words(n_old + n_new, m) words; words of
+ *         groups before n_old / 8 are not touched
+ * Errors: as bolt_encode, plus SHAPE (n_old < 0). */
+BOLT_API bolt_status bolt_encode_append(const float* X, int64_t n_new, int j, int64_t ldx, const float* C, int m,
+                                        uint32_t* codes, int64_t n_old, bolt_stream_t stream);
+
 /* Pack flat codes u8 [n][m] (values masked to 4 bits) into layout v1, and back. */
 BOLT_API bolt_status bolt_pack_codes(const uint8_t* flat, int64_t n, int m, uint32_t* codes,
                             bolt_stream_t stream);

@@ -71,6 +71,45 @@ def encode(X: torch.Tensor, C: torch.Tensor, out: torch.Tensor | None = None) ->
     return out
 
 
+def encode_append(X: torch.Tensor, C: torch.Tensor, codes: torch.Tensor, n_old: int) -> torch.Tensor:
+    """Encode-on-write: append the rows of X (fp32 [n_new][J]) to `codes`, which
+    holds n_old rows and has room for codes_words(n_old + n_new, M) words;
+    afterwards codes == encode(all rows) bit for bit (bolt_encode_append)."""
+    _cuda(X, "X", torch.float32)
+    _cuda(C, "C", torch.float32)
+    _cuda(codes, "codes", torch.uint32)
+    n_new, j = X.shape
+    m = C.shape[0]
+    if codes.numel() < codes_words(n_old + n_new, m):
+        raise ValueError(f"codes holds {codes.numel()} words, {codes_words(n_old + n_new, m)} needed")
+    _lib.call("bolt_encode_append", X.data_ptr(), n_new, j, j, C.data_ptr(), m, codes.data_ptr(), n_old,
+              _stream(X.device))
+    return codes
+
+
+class CodeBuffer:
+    """A live, growable layout-v1 code store for streaming encode-on-write
+    (SURVEY 8(f4)): append() encodes new rows straight into the buffer
+    (capacity doubles when full); `codes` / `n` feed topk / scan directly."""
+
+    def __init__(self, m: int, device, capacity: int = 1 << 16):
+        self.m, self.n = m, 0
+        self._buf = torch.zeros(codes_words(max(capacity, 8), m), dtype=torch.uint32, device=device)
+
+    @property
+    def codes(self) -> torch.Tensor:
+        return self._buf[:codes_words(self.n, self.m)]
+
+    def append(self, X: torch.Tensor, C: torch.Tensor) -> None:
+        need = codes_words(self.n + X.shape[0], self.m)
+        if need > self._buf.numel():
+            grown = torch.zeros(max(need, 2 * self._buf.numel()), dtype=torch.uint32, device=self._buf.device)
+            grown[:self._buf.numel()] = self._buf
+            self._buf = grown
+        encode_append(X, C, self._buf, self.n)
+        self.n += X.shape[0]
+
+
 def pack_codes(flat: torch.Tensor) -> torch.Tensor:
     _cuda(flat, "flat", torch.uint8)
     n, m = flat.shape

@@ -160,6 +160,22 @@ bolt_status bolt_encode(const float* X, int64_t n, int j, int64_t ldx, const flo
     return cuda_status(launch_encode(X, n, j, ldx, C, m, codes, (cudaStream_t)stream), "bolt_encode");
 }
 
+bolt_status bolt_encode_append(const float* X, int64_t n_new, int j, int64_t ldx, const float* C, int m,
+                               uint32_t* codes, int64_t n_old, bolt_stream_t stream) {
+    TRY(check_jm(j, m));
+    if (n_new < 0 || n_old < 0) return fail(BOLT_E_SHAPE, "n_new = %lld, n_old = %lld", (long long)n_new,
+                                            (long long)n_old);
+    if (ldx < j) return fail(BOLT_E_SHAPE, "ldx = %lld < j = %d", (long long)ldx, j);
+    if (j > 2048) return fail(BOLT_E_SHAPE, "j = %d > 2048 (centroids must fit in shared memory)", j);
+    if (n_new == 0) return BOLT_OK;
+    if (!X || !C || !codes) return fail(BOLT_E_NULL, "bolt_encode_append: NULL pointer");
+    if (!aligned(C, 16)) return fail(BOLT_E_ALIGN, "bolt_encode_append: C must be 16-byte aligned");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_encode_append(X, n_new, j, ldx, C, m, codes, n_old, (cudaStream_t)stream),
+                       "bolt_encode_append");
+}
+
 bolt_status bolt_pack_codes(const uint8_t* flat, int64_t n, int m, uint32_t* codes,
                             bolt_stream_t stream) {
     TRY(check_m(m));

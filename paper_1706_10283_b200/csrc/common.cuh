@@ -97,6 +97,8 @@ struct ScanArgs {
 namespace bolt {
 cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,
                           uint32_t* codes, cudaStream_t s);
+cudaError_t launch_encode_append(const float* X, int64_t n_new, int j, int64_t ldx, const float* C, int m,
+                                 uint32_t* codes, int64_t n_old, cudaStream_t s);
 cudaError_t launch_pack(const uint8_t* flat, int64_t n, int m, uint32_t* codes, cudaStream_t s);
 cudaError_t launch_unpack(const uint32_t* codes, int64_t n, int m, uint8_t* flat, cudaStream_t s);
 

@@ -267,6 +267,50 @@ cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const f
     return cudaGetLastError();
 }
 
+// Streaming append: the h < 8 rows that complete a partial layout-v1 group.
+// Thread c encodes codebook c of those rows with encode_kernel's scalar
+// arithmetic (x + (-c), then fma; ascending dimensions; lowest index on
+// ties) and rewrites the group's word c keeping the nibbles below `pos`.
+__global__ void append_head_kernel(const float* __restrict__ X, int h, int j, int64_t ldx,
+                                   const float* __restrict__ C, int m, uint32_t* __restrict__ word, int pos) {
+    const int c = threadIdx.x;
+    if (c >= m) return;
+    const int L = j / m;
+    uint32_t bits = 0;
+    for (int r = 0; r < h; ++r) {
+        const float* x = X + (int64_t)r * ldx + c * L;
+        float best = 0.f;
+        uint32_t arg = 0;
+        for (int k = 0; k < kK; ++k) {
+            const float* cc = C + ((int64_t)c * kK + k) * L;
+            float d = 0.f;
+            for (int t = 0; t < L; ++t) {
+                const float diff = __fadd_rn(x[t], -cc[t]);
+                d = __fmaf_rn(diff, diff, d);
+            }
+            if (k == 0 || d < best) { best = d; arg = (uint32_t)k; }
+        }
+        bits |= arg << (4 * (pos + r));
+    }
+    const uint32_t keep = pos == 0 ? 0u : (0xFFFFFFFFu >> (32 - 4 * pos));
+    word[c] = (word[c] & keep) | bits;
+}
+
+cudaError_t launch_encode_append(const float* X, int64_t n_new, int j, int64_t ldx, const float* C, int m,
+                                 uint32_t* codes, int64_t n_old, cudaStream_t s) {
+    if (n_new == 0) return cudaSuccess;
+    const int pos = (int)(n_old % kRowsPerWord);
+    const int64_t h = pos == 0 ? 0 : min64(kRowsPerWord - pos, n_new);
+    if (h > 0) {
+        append_head_kernel<<<1, ((m + 31) / 32) * 32, 0, s>>>(X, (int)h, j, ldx, C, m,
+                                                               codes + (n_old / kRowsPerWord) * m, pos);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (n_new == h) return cudaSuccess;
+    return launch_encode(X + h * ldx, n_new - h, j, ldx, C, m, codes + ((n_old + h) / kRowsPerWord) * m, s);
+}
+
 cudaError_t launch_pack(const uint8_t* flat, int64_t n, int m, uint32_t* codes, cudaStream_t s) {
     int64_t total = ceil_div(n, kRowsPerWord) * m;
     if (total == 0) return cudaSuccess;

@@ -1,4 +1,4 @@
-"""Row-sharded multi-GPU search.
+"""Multi-GPU search: row-sharded and query-sharded (8(f4)).
 
 Database rows shard naturally: every (query, vector) distance is independent,
 so rank r scans its contiguous shard [r0, r1) (whole layout-v1 groups, r0 % 8
@@ -43,3 +43,41 @@ def sharded_topk(codes_shard: torch.Tensor, n_shard: int, qluts: torch.Tensor, k
     if dist.get_world_size(group) == 1:
         return local
     return topk_merge(gather_keys(local, group))
+
+
+def query_range(nq: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous query slice of `rank` for the query-sharded mode."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    per = -(-nq // world)
+    q0 = min(rank * per, nq)
+    return q0, min(q0 + per, nq)
+
+
+def gather_query_slices(local: torch.Tensor, nq: int, group=None) -> torch.Tensor:
+    """Each rank's [q1 - q0][k] keys (its query_range slice) -> [nq][k] on every
+    rank: one all_gather_into_tensor of equal, padded slices."""
+    world = dist.get_world_size(group)
+    per = -(-nq // world)
+    k = local.shape[1]
+    pad = torch.full((per, k), -1, dtype=torch.int64, device=local.device)
+    pad[:local.shape[0]] = local.contiguous().view(torch.int64)
+    out = torch.empty((world * per, k), dtype=torch.int64, device=local.device)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    return out[:nq].view(torch.uint64)
+
+
+def query_sharded_topk(codes: torch.Tensor, n: int, qluts: torch.Tensor, k: int, metric, group=None,
+                       variant: int = 0) -> torch.Tensor:
+    """Replicated database, queries split over the ranks: rank r
+    scans all n rows for its query slice, so no merge is needed -- the only
+    exchange is gathering the disjoint result slices.  Pays off when the codes
+    fit on every GPU (c5's 0.8 GB does) and the queries outnumber the ranks."""
+    from . import topk
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    q0, q1 = query_range(qluts.shape[0], world, rank)
+    local = topk(codes, n, qluts[q0:q1].contiguous(), k, metric, variant=variant) if q1 > q0 else \
+        torch.empty((0, k), dtype=torch.uint64, device=codes.device)
+    if world == 1:
+        return local
+    return gather_query_slices(local, qluts.shape[0], group)

@@ -64,3 +64,42 @@ def test_shard_range_properties():
             for r0, r1 in ranges:
                 assert r0 % 8 == 0 or r0 == n
                 assert r0 <= r1
+
+
+def _qworker(rank, world, port, n, m, nq, k, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle
+        from paper_1706_10283_b200.dist import gather_query_slices, query_range
+        flat = G.random_codes(n, m, 3)
+        ql = G.random_qluts(nq, m, 4, hi=16)
+        q0, q1 = query_range(nq, world, rank)
+        local = oracle.topk(flat, ql[q0:q1], k, 0) if q1 > q0 else np.zeros((0, k), np.uint64)
+        res = gather_query_slices(torch.from_numpy(local), nq).numpy()
+        np.save(os.path.join(out_dir, f"q{rank}.npy"), res)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nq", [7, 1, 10])
+def test_query_sharded_gather_equals_whole(tmp_path, orc, nq):
+    """Replicated database, queries split over the ranks: the
+    gathered slices equal the single-process top-k; no merge is involved."""
+    world, n, m, k = 2, 900, 8, 6
+    port = _free_port()
+    mp.start_processes(_qworker, args=(world, port, n, m, nq, k, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    whole = orc.topk(G.random_codes(n, m, 3), G.random_qluts(nq, m, 4, hi=16), k, 0)
+    for r in range(world):
+        np.testing.assert_array_equal(np.load(tmp_path / f"q{r}.npy"), whole)
+
+
+def test_query_range_properties():
+    from paper_1706_10283_b200.dist import query_range
+    for nq in [0, 1, 5, 64, 65536, 10001]:
+        for world in [1, 2, 3, 8]:
+            rs = [query_range(nq, world, r) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == nq
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))

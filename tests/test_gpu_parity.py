@@ -473,6 +473,47 @@ def test_c5_full_size_sampled(bolt, orc):
     np.testing.assert_array_equal(keys[qs], orc.topk(gcodes, qlh, cfg5.k, 0))
 
 
+# ------------------------------------------- streaming encode-on-write (f4)
+@pytest.mark.parametrize("pieces", [[1, 7, 8, 3, 500, 1, 2000, 9, 13], [8, 8, 16], [5], [3, 3, 3, 3, 3, 3, 3, 3, 3]])
+def test_encode_append_equals_encode(bolt, orc, pieces):
+    """Appending rows in pieces (partial layout-v1 groups included) gives the
+    codes of encoding all rows at once, bit for bit, and those match the
+    oracle up to near-ties."""
+    import torch
+    cfg = G.CONFIGS["c2"]
+    n = sum(pieces)
+    X = G.database(cfg, n, start=11)
+    train = G.training(cfg, 4000)
+    C = orc.fit(train, cfg.m, G.kmeans_init_all(cfg, len(train)), 2)
+    whole = host(bolt.encode(dev(X), dev(C)))
+    buf = torch.full((bolt.codes_words(n, cfg.m),), 0xFFFFFFFF, dtype=torch.int64).to(torch.uint32).cuda()
+    n_old = 0
+    for p in pieces:
+        bolt.encode_append(dev(X[n_old:n_old + p]), dev(C), buf, n_old)
+        n_old += p
+    got = host(buf)
+    # words of the last group past row n: encode writes zero nibbles there
+    np.testing.assert_array_equal(got, whole)
+    _encode_check(bolt, orc, X, C)
+
+
+def test_code_buffer_grows_and_searches(bolt, orc):
+    import torch
+    cfg = G.CONFIGS["c2"]
+    X = G.database(cfg, 3001, start=5)
+    train = G.training(cfg, 4000)
+    C = orc.fit(train, cfg.m, G.kmeans_init_all(cfg, len(train)), 2)
+    a, b, _ = orc.fit_quantizer(G.calibration(cfg, train)[:100], C, 0)
+    cb = bolt.CodeBuffer(cfg.m, torch.device("cuda"), capacity=64)
+    for r0 in range(0, 3001, 777):
+        cb.append(dev(X[r0:r0 + 777]), dev(C))
+    assert cb.n == 3001
+    np.testing.assert_array_equal(host(cb.codes), host(bolt.encode(dev(X), dev(C))))
+    ql = bolt.build_quantized_luts(dev(G.queries(cfg, 7)), dev(C), 0, float(a), dev(b))
+    keys = host(bolt.topk(cb.codes, cb.n, ql, 10, 0))
+    np.testing.assert_array_equal(keys, orc.topk(orc.unpack_v1(host(cb.codes), 3001, cfg.m), host(ql), 10, 0))
+
+
 # ------------------------------------------------------- offline fit (f1)
 @pytest.mark.parametrize("cfg_name,n", [("c1", 10_000), ("c2", 20_000), ("c4", 5_000)])
 def test_kmeans_gpu_equals_oracle(bolt, orc, cfg_name, n):
