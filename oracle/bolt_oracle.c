@@ -349,6 +349,56 @@ void oracle_topk(const uint8_t* codes, int64_t n, int M, const uint8_t* qluts, i
     }
 }
 
+/* --------------------------------------------------------------- O13 -- */
+/* "Bolt No Quantize": the scan with the unquantized
+ * tables, out[i*nq + q] = sum_m D[q][m][i_m] with D the fp32 tables.  R17:
+ * summed in fp32, in ascending m from 0.0f -- the paper fixes no precision for
+ * this variant, so the oracle takes the kernel's, and a top-k decided by these
+ * sums is then exact (the near-tie rule of the parity contract). */
+void oracle_scan_f32(const uint8_t* codes, int64_t n, int M, const float* luts, int64_t nq, float* out) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t q = 0; q < nq; ++q) {
+            float acc = 0.0f;
+            for (int m = 0; m < M; ++m) acc = acc + luts[(q * M + m) * K + codes[i * M + m]];
+            out[i * nq + q] = acc;
+        }
+}
+
+/* O14: key of an fp32 distance (R18): the float's bits mapped to an unsigned
+ * order-preserving code (negative: all bits flipped; else the sign bit set),
+ * inverted for the dot product (larger is better), in the high 32 bits; the
+ * global index (< 2^32) in the low 32: ties by lower index. */
+static uint64_t make_key_f32(float v, int64_t gidx, int metric) {
+    uint32_t u;
+    memcpy(&u, &v, sizeof u);
+    uint32_t ord = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    if (metric != ORACLE_L2SQ) ord = ~ord;
+    return ((uint64_t)ord << 32) | (uint64_t)gidx;
+}
+
+/* k smallest fp32 keys per query, ascending; UINT64_MAX padding when k > n. */
+void oracle_topk_f32(const uint8_t* codes, int64_t n, int M, const float* luts, int64_t nq, int k, int metric,
+                     int64_t index_base, uint64_t* keys) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t q = 0; q < nq; ++q) {
+        uint64_t* best = keys + q * k;
+        for (int r = 0; r < k; ++r) best[r] = UINT64_MAX;
+        for (int64_t i = 0; i < n; ++i) {
+            float acc = 0.0f;
+            for (int m = 0; m < M; ++m) acc = acc + luts[(q * M + m) * K + codes[i * M + m]];
+            uint64_t key = make_key_f32(acc, index_base + i, metric);
+            if (key >= best[k - 1]) continue;
+            int r = k - 1;
+            while (r > 0 && best[r - 1] > key) {
+                best[r] = best[r - 1];
+                --r;
+            }
+            best[r] = key;
+        }
+    }
+}
+
 /* ---------------------------------------------------------------- O9 -- */
 static int cmp_u64(const void* pa, const void* pb) {
     uint64_t a = *(const uint64_t*)pa, b = *(const uint64_t*)pb;

@@ -49,6 +49,8 @@ def lib():
             "oracle_kmeans_subspace": ([P, i64, i32, i32, i32, P, i32, P, P], None),
             "oracle_scan": ([P, i64, i32, P, i64, P], None),
             "oracle_topk": ([P, i64, i32, P, i64, i32, i32, i64, P], None),
+            "oracle_scan_f32": ([P, i64, i32, P, i64, P], None),
+            "oracle_topk_f32": ([P, i64, i32, P, i64, i32, i32, i64, P], None),
             "oracle_merge": ([P, i32, i64, i32, P], None),
             "oracle_dequant": ([P, i64, f32, P, i32, P], None),
             "oracle_unpack_v1": ([P, i64, i32, P], None),
@@ -162,6 +164,43 @@ def topk(codes, qluts, k: int, metric: int, index_base: int = 0):
     keys = np.empty((nq, k), np.uint64)
     lib().oracle_topk(_p(codes), n, M, _p(qluts), nq, int(k), int(metric), int(index_base), _p(keys))
     return keys
+
+
+def scan_f32(codes, luts32):
+    """O13 (Bolt No Quantize): flat codes u8 [n][M], fp32 tables [nq][M][16] ->
+    fp32 [n][nq], summed in fp32 in ascending m (R17)."""
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    luts32 = np.ascontiguousarray(luts32, dtype=np.float32)
+    n, M = codes.shape
+    nq = luts32.shape[0]
+    out = np.empty((n, nq), np.float32)
+    lib().oracle_scan_f32(_p(codes), n, M, _p(luts32), nq, _p(out))
+    return out
+
+
+def topk_f32(codes, luts32, k: int, metric: int, index_base: int = 0):
+    """O14: -> u64 keys [nq][k] (R18: order-preserving float code << 32 | index)."""
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    luts32 = np.ascontiguousarray(luts32, dtype=np.float32)
+    n, M = codes.shape
+    nq = luts32.shape[0]
+    keys = np.empty((nq, k), np.uint64)
+    lib().oracle_topk_f32(_p(codes), n, M, _p(luts32), nq, int(k), int(metric), int(index_base), _p(keys))
+    return keys
+
+
+def keys_split_f32(keys, metric: int):
+    """u64 keys (R18) -> (fp32 values, int64 indices; -1 for padding)."""
+    keys = np.asarray(keys, dtype=np.uint64)
+    ord_ = (keys >> np.uint64(32)).astype(np.uint32)
+    if metric == DOT:
+        ord_ = ~ord_
+    u = np.where(ord_ & np.uint32(0x80000000), ord_ & np.uint32(0x7FFFFFFF), ~ord_).astype(np.uint32)
+    vals = u.view(np.float32)
+    idx = (keys & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    pad = keys == np.uint64(0xFFFFFFFFFFFFFFFF)
+    idx[pad] = -1
+    return vals, idx
 
 
 def merge(shard_keys):

@@ -347,3 +347,63 @@ def test_lemmas_3_4(orc):
     d1 = np.linalg.norm(Q64[:, None] - X64[None], axis=2)
     d2 = np.linalg.norm(Q64[:, None] - xh[None], axis=2)
     assert (np.abs(d1 - d2) <= r[None] + 1e-12).all()
+
+
+# ------------------------------------------------- Bolt No Quantize (f3, O13/O14)
+@pytest.mark.parametrize("metric", [0, 1])
+def test_scan_f32_within_summation_bound_and_reconstruction(orc, metric):
+    """O13 against the mathematics: the fp32 running sum of M fp32 table
+    entries differs from the exact (fp64) sum of the same entries by at most
+    (M - 1) u sum|entries| (u = 2^-24, recursive summation bound); and with
+    the exact tables rounded to fp32, the scan of a vector's codes is its
+    reconstruction's dense distance within that bound plus the rounding of
+    the M entries."""
+    M, L = 8, 4
+    C = centroid_bank(M, L, 141)
+    X = G.random_floats((64, M * L), 142)
+    Q = G.random_floats((5, M * L), 143)
+    codes = orc.encode(X, C)
+    D64 = orc.luts(Q, C, metric)
+    D32 = D64.astype(np.float32)
+    got = orc.scan_f32(codes, D32).astype(np.float64)
+    terms = np.stack([D32[:, m, :][:, codes[:, m]] for m in range(M)]).astype(np.float64)  # [M][nq][n]
+    exact = terms.sum(0).T
+    bound = (M - 1) * 2.0**-24 * np.abs(terms).sum(0).T
+    assert (np.abs(got - exact) <= bound + 1e-30).all()
+    xhat = np.concatenate([C[m][codes[:, m]] for m in range(M)], axis=1).astype(np.float64)
+    Q64 = Q.astype(np.float64)
+    dense = (((Q64[:, None, :] - xhat[None]) ** 2).sum(-1) if metric == 0 else Q64 @ xhat.T).T
+    round_err = 2.0**-24 * np.abs(np.stack([D64[:, m, :][:, codes[:, m]] for m in range(M)])).sum(0).T
+    assert (np.abs(got - dense) <= bound + round_err + 1e-12).all()
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+def test_topk_f32_reduces_to_quantized_topk(orc, metric):
+    """O14 against O8: with integer tables (exact in fp32, sums <= 255 M exact)
+    the fp32 top-k ranks exactly as the u8 top-k -- same indices, same values
+    -- including the heavy ties of small tables (lower index first)."""
+    n, M, nq = 700, 8, 6
+    codes = G.random_codes(n, M, 170)
+    for hi in (4, 256):
+        ql = G.random_qluts(nq, M, 171 + hi, hi=hi)
+        for k in (1, 10, n, n + 5):
+            ref_v, ref_i = orc.keys_split(orc.topk(codes, ql, k, metric, index_base=33), metric)
+            v, i = orc.keys_split_f32(orc.topk_f32(codes, ql.astype(np.float32), k, metric, index_base=33), metric)
+            np.testing.assert_array_equal(i, ref_i)
+            ok = ref_i >= 0
+            np.testing.assert_array_equal(v[ok], ref_v[ok].astype(np.float32))
+
+
+def test_topk_f32_order_on_signed_values(orc):
+    """R18 on negative / mixed-sign sums (dot tables): the keys sort as the
+    floats do -- checked against numpy's stable argsort of the O13 sums."""
+    n, M, nq = 300, 4, 3
+    codes = G.random_codes(n, M, 180)
+    luts = G.random_floats((nq, M, 16), 181, 3.0)
+    s = orc.scan_f32(codes, luts)
+    for metric in (0, 1):
+        v, idx = orc.keys_split_f32(orc.topk_f32(codes, luts, n, metric), metric)
+        for q in range(nq):
+            order = np.argsort(s[:, q] if metric == 0 else -s[:, q], kind="stable")
+            np.testing.assert_array_equal(idx[q], order)
+            np.testing.assert_array_equal(v[q], s[order, q])
