@@ -683,6 +683,73 @@ def run_c5(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------- No Quantize (f3)
+def run_noquant(args):
+    """SURVEY 8(f3) "Bolt No Quantize" on c2: step = encode + fp32
+    tables (bolt_build_luts) + fp32-table scan with fused top-10
+    (bolt_topk_f32).  The paper keeps the variant only as an accuracy
+    reference ("it sacrifices Bolt's high speed"); its roofline is the
+    shared-memory lookup rate: one 4-byte LDS per lookup, M per distance,
+    at 32 lookups / clk / SM (128 B/clk crossbar, B300_MICROARCH.md)."""
+    import torch
+
+    import paper_1706_10283_b200 as bolt
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    cfg = G.CONFIGS["c2"]
+    n, nq, k, metric = args.n or cfg.n, args.nq or cfg.nq, cfg.k, cfg.metrics[0]
+    model = c2_model(bolt, dev)
+    Xd = torch.from_numpy(G.database(cfg, n)).to(dev)
+    Qd = torch.from_numpy(G.queries(cfg, nq)).to(dev)
+    codes = torch.empty(bolt.codes_words(n, cfg.m), dtype=torch.uint32, device=dev)
+    keys = torch.empty((nq, k), dtype=torch.uint64, device=dev)
+    luts = {}
+
+    def step():
+        bolt.encode(Xd, model.C, out=codes)
+        luts["D"] = bolt.build_luts(Qd, model.C, metric)
+        bolt.topk_f32(codes, n, luts["D"], k, metric, out=keys)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    clk = ClockSampler(0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            bolt.topk_f32(codes, n, luts["D"], k, metric, out=keys)
+        s1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    scan_ms = s0.elapsed_time(s1) / args.steps
+    peaks, peak_src = measured_peaks()
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    lookups = n * nq * cfg.m / (scan_ms * 1e-3)
+    peak = 148 * 32 * sm_mhz * 1e6
+    out = {"metric": METRIC, "value": round(n * nq / (ms * 1e-3) / 1e9, 4), "unit": UNIT, "n_gpus": 1,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (seeded SIFT1M-like Gaussian mixture, SURVEY 8(d) c2 recipe)",
+           "config": {"workload": f"c2 No Quantize (P:L390): N={n}, J=128, M={cfg.m}, Q={nq}, squared L2, top-{k} "
+                                  "over fp32 tables; step = encode + fp32 tables + fp32 scan/top-k",
+                      "n_per_gpu": n, "nq": nq, "m": cfg.m, "k": k},
+           "roofline": {"bound": "smem", "achieved": round(lookups / 1e12, 3), "peak": round(peak / 1e12, 3),
+                        "unit": "T lookups/s", "frac": round(lookups / peak, 4), "traffic": None,
+                        "peak_source": f"148 SM x 32 LDS lanes/clk x {sm_mhz:.0f} MHz ({peak_src} sm_max_mhz)",
+                        "kernel": "bolt_topk_f32", "kernel_ms": round(scan_ms, 4)},
+           "clocks": clk.summary(), "gpu_launches": args.steps * 4}
+    print(json.dumps(out))
+
+
 # ------------------------------------------------------------------ sweep
 SWEEP_Q = (1, 2, 4, 8, 16, 32, 64, 128, 256)
 
@@ -788,6 +855,8 @@ if __name__ == "__main__":
         run_sweep(a)
     elif a.config == "c5" and a.impl != "reference":
         run_c5(a)
+    elif a.config == "c2nq" and a.impl != "reference":
+        run_noquant(a)
     elif a.impl == "reference":
         run_reference(a)
     else:

@@ -198,6 +198,28 @@ BOLT_API bolt_status bolt_topk_merge(const uint64_t* keys, int w, int64_t nq, in
 BOLT_API bolt_status bolt_keys_split(const uint64_t* keys, int64_t count, bolt_metric metric,
                             uint16_t* vals, int64_t* idx, bolt_stream_t stream);
 
+/* ------------------------------------------- Bolt No Quantize (fp32 tables) */
+/* The variant of P:L390 that skips table quantization: the
+ * running total of P:L224-231 over the fp32 tables D of bolt_build_luts,
+ * summed in fp32 in ascending codebook order from 0 (R17).
+ *   luts [nq][m][16] fp32 (4 B aligned); codes layout v1 for n rows (16 B aligned)
+ *   out  fp32, out[i*ldo + q], ldo >= nq
+ * Errors: NULL, SHAPE (m not in 1..64, n or nq < 0, ldo < nq), ALIGN. */
+BOLT_API bolt_status bolt_scan_f32(const uint32_t* codes, int64_t n, int m, const float* luts, int64_t nq,
+                                   float* out, int64_t ldo, bolt_stream_t stream);
+/* k best per query of those fp32 totals by the 64-bit key (R18)
+ *   key = (ord(v) << 32) | (index_base + i), ord = the float's order-preserving
+ *   unsigned code (negative: bits flipped, else sign bit set), inverted for DOT;
+ * ascending, best first, ties by the lower index.  1 <= k <= 32;
+ * index_base + n <= 2^32.  ws >= bolt_topk_f32_workspace_bytes(n, m, nq, k). */
+BOLT_API size_t bolt_topk_f32_workspace_bytes(int64_t n, int m, int64_t nq, int k);
+BOLT_API bolt_status bolt_topk_f32(const uint32_t* codes, int64_t n, int m, const float* luts, int64_t nq, int k,
+                                   bolt_metric metric, int64_t index_base, uint64_t* out_keys, void* ws,
+                                   size_t ws_bytes, bolt_stream_t stream);
+/* Split R18 keys into fp32 values and global indices (-1 for padding). */
+BOLT_API bolt_status bolt_keys_split_f32(const uint64_t* keys, int64_t count, bolt_metric metric, float* vals,
+                                         int64_t* idx, bolt_stream_t stream);
+
 /* ------------------------------------------------- end-to-end (host buffers) */
 /* One search from HOST inputs: copies X and Q host->device, encodes X (h),
  * builds quantized tables (g), runs the top-k scan, copies the keys

@@ -242,6 +242,45 @@ def keys_split(keys: torch.Tensor, metric):
     return vals, idx
 
 
+# ------------------------------------------- Bolt No Quantize (fp32 tables)
+def scan_f32(codes: torch.Tensor, n: int, luts: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """P:L390's "Bolt No Quantize": fp32 [n][nq] totals of the fp32 tables
+    (build_luts) summed in fp32, ascending codebooks (bolt_scan_f32)."""
+    _cuda(codes, "codes", torch.uint32)
+    _cuda(luts, "luts", torch.float32)
+    nq, m, _ = luts.shape
+    if out is None:
+        out = torch.empty((n, nq), dtype=torch.float32, device=codes.device)
+    _lib.call("bolt_scan_f32", codes.data_ptr(), n, m, luts.data_ptr(), nq, out.data_ptr(), out.stride(0),
+              _stream(codes.device))
+    return out
+
+
+def topk_f32(codes: torch.Tensor, n: int, luts: torch.Tensor, k: int, metric, index_base: int = 0,
+             out: torch.Tensor | None = None) -> torch.Tensor:
+    """u64 keys [nq][k] of the fp32 totals (R18), ascending; k <= 32."""
+    _cuda(codes, "codes", torch.uint32)
+    _cuda(luts, "luts", torch.float32)
+    nq, m, _ = luts.shape
+    if out is None:
+        out = torch.empty((nq, k), dtype=torch.uint64, device=codes.device)
+    wsb = _lib.load().bolt_topk_f32_workspace_bytes(n, m, nq, k)
+    ws = torch.empty(max(int(wsb), 8), dtype=torch.uint8, device=codes.device)
+    _lib.call("bolt_topk_f32", codes.data_ptr(), n, m, luts.data_ptr(), nq, k, _metric(metric), index_base,
+              out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(codes.device))
+    return out
+
+
+def keys_split_f32(keys: torch.Tensor, metric):
+    """R18 keys -> (fp32 values, global indices int64; -1 for padding)."""
+    _cuda(keys, "keys", torch.uint64)
+    vals = torch.empty(keys.shape, dtype=torch.float32, device=keys.device)
+    idx = torch.empty(keys.shape, dtype=torch.int64, device=keys.device)
+    _lib.call("bolt_keys_split_f32", keys.data_ptr(), keys.numel(), _metric(metric), vals.data_ptr(),
+              idx.data_ptr(), _stream(keys.device))
+    return vals, idx
+
+
 # --------------------------------------------------------- end-to-end (host)
 class HostSearch:
     """Host-buffer search: H2D of X and Q, encode, fused tables, top-k, D2H of

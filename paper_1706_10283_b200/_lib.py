@@ -42,6 +42,10 @@ SIGNATURES = {
     "bolt_topk_ex": ([_P, _I64, _I32, _P, _I64, _I32, _I32, _I64, _P, _P, _SZ, _I32, _P], _I32),
     "bolt_topk_merge": ([_P, _I32, _I64, _I32, _P, _P], _I32),
     "bolt_keys_split": ([_P, _I64, _I32, _P, _P, _P], _I32),
+    "bolt_scan_f32": ([_P, _I64, _I32, _P, _I64, _P, _I64, _P], _I32),
+    "bolt_topk_f32_workspace_bytes": ([_I64, _I32, _I64, _I32], ctypes.c_size_t),
+    "bolt_topk_f32": ([_P, _I64, _I32, _P, _I64, _I32, _I32, _I64, _P, _P, ctypes.c_size_t, _P], _I32),
+    "bolt_keys_split_f32": ([_P, _I64, _I32, _P, _P, _P], _I32),
     "bolt_search_host_workspace_bytes": ([_I64, _I32, _I32, _I64, _I32], _SZ),
     "bolt_search_host": ([_P, _I64, _I32, _P, _I64, _P, _I32, _I32, _F32, _P, _I32, _P, _P, _SZ, _P], _I32),
     "bolt_search_host_pipelined_workspace_bytes": ([_I64, _I32, _I32, _I64, _I32, _I32], _SZ),

@@ -160,6 +160,72 @@ bolt_status bolt_encode(const float* X, int64_t n, int j, int64_t ldx, const flo
     return cuda_status(launch_encode(X, n, j, ldx, C, m, codes, (cudaStream_t)stream), "bolt_encode");
 }
 
+// ---- Bolt No Quantize (scan_f32.cu)
+static bolt_status f32_common(const uint32_t* codes, int64_t n, int m, const float* luts, int64_t nq) {
+    TRY(check_m(m));
+    if (n < 0 || nq < 0) return fail(BOLT_E_SHAPE, "n or nq < 0");
+    if (n > 0 && nq > 0) {
+        if (!codes || !luts) return fail(BOLT_E_NULL, "codes/luts NULL");
+        if (!aligned(codes, 16)) return fail(BOLT_E_ALIGN, "codes must be 16-byte aligned");
+        if (!aligned(luts, 4)) return fail(BOLT_E_ALIGN, "luts must be 4-byte aligned");
+    }
+    return BOLT_OK;
+}
+
+bolt_status bolt_scan_f32(const uint32_t* codes, int64_t n, int m, const float* luts, int64_t nq, float* out,
+                          int64_t ldo, bolt_stream_t stream) {
+    TRY(f32_common(codes, n, m, luts, nq));
+    if (ldo < nq) return fail(BOLT_E_SHAPE, "ldo < nq");
+    if (n == 0 || nq == 0) return BOLT_OK;
+    if (!out) return fail(BOLT_E_NULL, "out NULL");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_scan_f32(codes, n, m, luts, nq, out, ldo, (cudaStream_t)stream), "bolt_scan_f32");
+}
+
+size_t bolt_topk_f32_workspace_bytes(int64_t n, int m, int64_t nq, int k) {
+    if (n <= 0 || nq <= 0 || k < 1 || k > 32 || m < 1 || m > kMaxM) return 0;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    return (size_t)topk_f32_parts(n, nq, sms) * nq * k * sizeof(uint64_t);
+}
+
+bolt_status bolt_topk_f32(const uint32_t* codes, int64_t n, int m, const float* luts, int64_t nq, int k,
+                          bolt_metric metric, int64_t index_base, uint64_t* out_keys, void* ws, size_t ws_bytes,
+                          bolt_stream_t stream) {
+    TRY(f32_common(codes, n, m, luts, nq));
+    if (k < 1 || k > 32) return fail(BOLT_E_SHAPE, "k = %d outside 1..32", k);
+    if (metric != BOLT_L2SQ && metric != BOLT_DOT) return fail(BOLT_E_RANGE, "metric %d", (int)metric);
+    if (index_base < 0 || index_base + n > (int64_t(1) << 32)) return fail(BOLT_E_RANGE, "index_base + n > 2^32");
+    if (nq == 0) return BOLT_OK;
+    if (!out_keys) return fail(BOLT_E_NULL, "out_keys NULL");
+    DevInfo d;
+    TRY(device_info(&d));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0)
+        return cuda_status(cudaMemsetAsync(out_keys, 0xFF, (size_t)nq * k * sizeof(uint64_t), s), "bolt_topk_f32");
+    const int parts = topk_f32_parts(n, nq, d.sms);
+    const size_t need = (size_t)parts * nq * k * sizeof(uint64_t);
+    if (!ws || ws_bytes < need) return fail(BOLT_E_WORKSPACE, "workspace of %zu bytes required, %zu given", need, ws_bytes);
+    if (!aligned(ws, 8)) return fail(BOLT_E_ALIGN, "workspace must be 8-byte aligned");
+    uint64_t* pk = static_cast<uint64_t*>(ws);
+    TRY(cuda_status(launch_topk_f32(codes, n, m, luts, nq, k, (int)metric, index_base, parts, pk, s),
+                    "bolt_topk_f32 scan"));
+    return cuda_status(launch_merge_many(pk, parts, nq, k, k, out_keys, s), "bolt_topk_f32 merge");
+}
+
+bolt_status bolt_keys_split_f32(const uint64_t* keys, int64_t count, bolt_metric metric, float* vals, int64_t* idx,
+                                bolt_stream_t stream) {
+    if (count < 0) return fail(BOLT_E_SHAPE, "count < 0");
+    if (count == 0) return BOLT_OK;
+    if (!keys) return fail(BOLT_E_NULL, "keys NULL");
+    DevInfo d;
+    TRY(device_info(&d));
+    return cuda_status(launch_keys_split_f32(keys, count, (int)metric, vals, idx, (cudaStream_t)stream),
+                       "bolt_keys_split_f32");
+}
+
 bolt_status bolt_encode_append(const float* X, int64_t n_new, int j, int64_t ldx, const float* C, int m,
                                uint32_t* codes, int64_t n_old, bolt_stream_t stream) {
     TRY(check_jm(j, m));

@@ -473,6 +473,55 @@ def test_c5_full_size_sampled(bolt, orc):
     np.testing.assert_array_equal(keys[qs], orc.topk(gcodes, qlh, cfg5.k, 0))
 
 
+# --------------------------------------------- Bolt No Quantize (f3, O13/O14)
+F32_SHAPES = [(1, 1, 1), (300, 8, 5), (1001, 16, 33), (4099, 32, 64), (257, 64, 7), (5000, 5, 40)]
+
+
+@pytest.mark.parametrize("n,m,nq", F32_SHAPES)
+def test_scan_f32_bit_exact(bolt, orc, n, m, nq):
+    """Same fp32 tables and codes: fp32 totals bit-identical to O13 (fp32,
+    ascending m); ragged n (partial groups), nq (partial query tiles), odd m."""
+    flat = G.random_codes(n, m, 300 + n)
+    luts = G.random_floats((nq, m, 16), 301 + nq, 10.0)
+    got = host(bolt.scan_f32(pack_on_gpu(bolt, flat), n, dev(luts)))
+    np.testing.assert_array_equal(got, orc.scan_f32(flat, luts))
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+@pytest.mark.parametrize("n,m,nq,k", [(5000, 16, 40, 10), (777, 8, 3, 32), (20, 4, 70, 30), (100_000, 16, 33, 1),
+                                      (3, 8, 2, 10)])
+def test_topk_f32_bit_exact(bolt, orc, metric, n, m, nq, k):
+    flat = G.random_codes(n, m, 400 + n)
+    luts = G.random_floats((nq, m, 16), 401 + nq, 10.0)
+    if metric == 0:
+        luts = np.abs(luts)  # distances
+    keys = bolt.topk_f32(pack_on_gpu(bolt, flat), n, dev(luts), k, metric, index_base=9)
+    ref = orc.topk_f32(flat, luts, k, metric, index_base=9)
+    np.testing.assert_array_equal(host(keys), ref)
+    v, i = bolt.keys_split_f32(keys, metric)
+    rv, ri = orc.keys_split_f32(ref, metric)
+    np.testing.assert_array_equal(host(i), ri)
+    np.testing.assert_array_equal(host(v)[ri >= 0], rv[ri >= 0])
+
+
+def test_topk_f32_ties_and_tables_from_model(bolt, orc):
+    """Integer tables (heavy ties; lower index first) and the model's own fp32
+    tables (build_luts) fed to both sides."""
+    n, m, nq = 3000, 16, 12
+    flat = G.random_codes(n, m, 17)
+    luts = G.random_qluts(nq, m, 18, hi=3).astype(np.float32)
+    np.testing.assert_array_equal(host(bolt.topk_f32(pack_on_gpu(bolt, flat), n, dev(luts), 20, 0)),
+                                  orc.topk_f32(flat, luts, 20, 0))
+    cfg = G.CONFIGS["c2"]
+    X = G.database(cfg, 5000)
+    train = G.training(cfg, 4000)
+    C = orc.fit(train, cfg.m, G.kmeans_init_all(cfg, len(train)), 2)
+    codes = bolt.encode(dev(X), dev(C))
+    D = bolt.build_luts(dev(G.queries(cfg, 9)), dev(C), 0)
+    np.testing.assert_array_equal(host(bolt.topk_f32(codes, 5000, D, 10, 0)),
+                                  orc.topk_f32(orc.unpack_v1(host(codes), 5000, cfg.m), host(D), 10, 0))
+
+
 # ------------------------------------------- streaming encode-on-write (f4)
 @pytest.mark.parametrize("pieces", [[1, 7, 8, 3, 500, 1, 2000, 9, 13], [8, 8, 16], [5], [3, 3, 3, 3, 3, 3, 3, 3, 3]])
 def test_encode_append_equals_encode(bolt, orc, pieces):
