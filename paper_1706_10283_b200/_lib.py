@@ -76,8 +76,8 @@ def load() -> ctypes.CDLL:
                               "`python -m paper_1706_10283_b200.build` (no CPU fallback exists)")
         lib = ctypes.CDLL(LIB_PATH)
         for name, (args, res) in SIGNATURES.items():
-            if name.startswith("bolt_debug_") and not hasattr(lib, name):
-                continue  # diagnostics absent from an older build (tools/ A/B runs)
+            if not hasattr(lib, name) and (name.startswith("bolt_debug_") or os.environ.get("BOLT_LIB")):
+                continue  # absent from an older build loaded for a tools/ A/B run
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = res
