@@ -76,7 +76,10 @@ typedef enum { BOLT_L2SQ = 0, BOLT_DOT = 1 } bolt_metric;
 typedef enum {
     BOLT_VARIANT_AUTO = 0,  /* library picks (documented in DESIGN.md) */
     BOLT_VARIANT_PRMT = 1,  /* CUDA-core PRMT byte-permute lookups */
-    BOLT_VARIANT_TC = 2     /* tcgen05 one-hot(codes) x table, kind::i8 */
+    BOLT_VARIANT_TC = 2,    /* tcgen05 one-hot(codes) x table, kind::i8 */
+    BOLT_VARIANT_TCS = 3    /* tcgen05 with the roles swapped for small query batches:
+                               vectors on the MMA's M side, nq <= 128 queries on N
+                               (top-k only, k <= 32, m in {8, 16, 32}) */
 } bolt_variant;
 
 /* ------------------------------------------------------------------ info */

@@ -129,6 +129,11 @@ int scan_tc_supported(int64_t n, int m, int64_t nq);
 cudaError_t launch_scan_tc(const ScanArgs& a, uint16_t* out16, float* out32, int64_t ldo, float inv_a, float b_sum,
                            int sms, cudaStream_t s);
 int topk_tc_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
+// swapped tcgen05 top-k for small query batches (vectors on the MMA M side)
+int topk_tcs_supported(int64_t n, int m, int64_t nq, int k);
+int topk_tcs_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
+cudaError_t launch_topk_tcs(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
+                            uint64_t* part_keys, cudaStream_t s);
 // part_keys: parts*nq*k keys followed by the shared threshold words (zeroed by the launch)
 cudaError_t launch_topk_tc(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
                            uint64_t* part_keys, int sms, cudaStream_t s);

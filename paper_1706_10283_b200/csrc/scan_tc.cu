@@ -95,15 +95,19 @@ constexpr int kPrefetch = 3;             // tiles of code words in flight per pr
 constexpr int kScratchStrideTopk = 20;
 constexpr int kScratchStrideFull = 32;
 
-template <int M, bool kFull = false>
+// QROWS: query rows of the table buffer per CTA (kQM, or kNQ/2 in the
+// swapped top-k); LIST_BYTES: the swapped top-k's per-warp lists (else the
+// scratch rows of the other modes)
+template <int M, bool kFull = false, int QROWS = kQM, int LIST_BYTES = 0>
 struct Cfg {
     static constexpr int SCRATCH_STRIDE = kFull ? kScratchStrideFull : kScratchStrideTopk;
     static constexpr int K = 16 * M;                      // bytes per row
     static constexpr int N = 256;                         // vectors per MMA tile (pair)
     static constexpr int NH = N / 2;                      // vectors per CTA (its half of B)
-    static constexpr int A_BYTES = kQM * K;
+    static constexpr int QR = QROWS;
+    static constexpr int A_BYTES = QROWS * K;
     static constexpr int B_BYTES = NH * K;                // one stage of this CTA's half of B
-    static constexpr int SCRATCH_BYTES = kEpilogue * SCRATCH_STRIDE * 4;
+    static constexpr int SCRATCH_BYTES = LIST_BYTES ? LIST_BYTES : kEpilogue * SCRATCH_STRIDE * 4;
     static constexpr int STAGES_RAW = (227 * 1024 - 256 - A_BYTES - SCRATCH_BYTES) / B_BYTES;
     static constexpr int STAGES = STAGES_RAW > 5 ? 5 : STAGES_RAW;
     static_assert(STAGES >= 2, "shared memory too small for a double-buffered B tile");
@@ -121,6 +125,9 @@ struct Cfg {
     // instruction descriptor: D s32 (bits 4-5 = 2), A/B u8 (format 0), K-major,
     // N >> 3 at bit 17, M >> 4 at bit 24 (M = 256 for the pair)
     static constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+    // swapped top-k: M = 256 vectors (A = one-hot), N = 2 QROWS queries (B = tables)
+    static constexpr uint32_t IDESC_SW = (2u << 4) | ((uint32_t)((2 * QROWS) >> 3) << 17) |
+                                         ((uint32_t)(256 >> 4) << 24);
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -244,6 +251,12 @@ __device__ __forceinline__ void tmem_ld16p(uint32_t taddr, uint32_t (&r)[16]) {
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
 }
+// 16 columns as 8 registers (same packing)
+__device__ __forceinline__ void tmem_ld8p(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.pack::16b.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // 32-bit shift with PTX clamping (shift amounts >= 32, including "negative"
@@ -341,14 +354,179 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sm
                  : "memory");
 }
 
-template <int M, bool kDot, int KMAX, int kOut = 0, bool kGroup = false>
+// ------------------------------------------------ swapped top-k epilogue
+// kOut = 3: vectors on the MMA M side (A = one-hot, 128 per CTA = TMEM
+// lanes), queries on N (B = tables of kNQ queries, kNQ/2 per CTA), so a
+// small query batch does not pad the MMA to 256 queries.  Warp (quad, half)
+// owns vectors 32 quad .. of its CTA (one per lane) and queries
+// [half QW, half QW + QW) of the tile (QW = kNQ / 2, registers).  One sorted
+// list of k <= 32 32-bit keys (kv' << IDX_BITS | local vector index) per
+// (warp, query) in shared memory; a packed SWAR test against per-query
+// thresholds (own k-th value, the query's shared word) finds candidates, and
+// the warp inserts them one at a time (lane l holds entry l).  Lists of a
+// query: 8 per CTA pair and row partition, merged afterwards.
+template <typename C, bool kDot, int kNQ>
+__device__ __forceinline__ void epilogue_swapped(const ScanArgs& a, int k, int64_t index_base, int64_t vbeg,
+                                                 int64_t vend, int ntiles, int part, int tq, uint32_t rank,
+                                                 int warp, int lane, uint32_t tmem, uint64_t* tfull,
+                                                 uint64_t* tempty, uint32_t* lists, uint64_t* part_keys,
+                                                 uint32_t* gthr_inv, int xmode) {
+    constexpr int QW = kNQ / 2;  // queries per warp
+    constexpr int NR = QW / 2;   // packed registers
+    constexpr int NW = (QW + 31) / 32;
+    const int quad = warp & 3, half = warp >> 2;
+    uint32_t* lst = lists + warp * QW * 32;  // [QW][32]
+    const int64_t qb = (int64_t)tq * kNQ + half * QW;  // first query of this warp
+    for (int e = lane; e < QW * 32; e += 32) lst[e] = 0xFFFFFFFFu;
+    __syncwarp();
+    // thresholds in kv' units (candidate iff kv' < thr); 0x7FFF = none (every
+    // value < 0x7FFF), 0 for queries past nq (never a candidate)
+    uint32_t thrp[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+        const uint32_t lo = qb + 2 * i < a.nq ? 0x7FFFu : 0u, hi = qb + 2 * i + 1 < a.nq ? 0x7FFFu : 0u;
+        thrp[i] = lo | (hi << 16);
+    }
+    uint32_t gw[NW];  // shared words (inverted 0xFFFF - T) of queries qb + lane + 32 w
+#pragma unroll
+    for (int w = 0; w < NW; ++w) gw[w] = 0;
+    const uint32_t tlane = (uint32_t)(quad * 32) << 16;
+    const uint32_t kvmax2 = C::KVMAX | (C::KVMAX << 16);
+    for (int tile = 0; tile < ntiles; ++tile) {
+        const int d = tile & 1;
+        mbar_wait(&tfull[d], (tile >> 1) & 1);
+        tc_fence_after();
+        uint32_t p[NR];
+        const uint32_t ta = tmem + tlane + (uint32_t)(d * kNQ + half * QW);
+        if (xmode & 8) {  // diagnostic: no TMEM reads
+#pragma unroll
+            for (int i = 0; i < NR; ++i) p[i] = 0x7FFF7FFFu;
+        } else if constexpr (QW == 16) {
+            uint32_t r[8];
+            tmem_ld8p(ta, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) p[i] = r[i];
+        } else {
+#pragma unroll
+            for (int c = 0; c < QW / 32; ++c) {
+                uint32_t r[16];
+                tmem_ld16p(ta + c * 32, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 16; ++i) p[c * 16 + i] = r[i];
+            }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+            if (rank == 0) mbar_arrive(&tempty[d]);
+            else mbar_arrive_cluster_relaxed(&tempty[d], 0);
+        }
+        if (xmode & 1) continue;  // diagnostic: load + release only
+        const int64_t vl = (int64_t)tile * C::N + rank * C::NH + quad * 32 + lane;  // local vector index
+        const bool vvalid = vbeg + vl < vend;
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+            if (kDot) p[i] = kvmax2 - p[i];  // kv' = KVMAX - acc per half (no borrow: acc <= KVMAX)
+            if (!vvalid) p[i] = 0x7FFF7FFFu;
+        }
+        // shared thresholds: re-read every 8 tiles, folded into thrp
+        if ((tile & 7) == 7) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const int64_t q = qb + lane + 32 * w;
+                uint32_t v = 0;
+                if (lane + 32 * w < QW && q < a.nq)
+                    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gthr_inv + q));
+                gw[w] = v;
+            }
+#pragma unroll
+            for (int i = 0; i < NR; ++i) {
+                // own k-th values from the lists (shared-memory broadcast reads)
+                const uint32_t k0 = lst[(2 * i) * 32 + k - 1], k1 = lst[(2 * i + 1) * 32 + k - 1];
+                const uint32_t o0 = k0 == 0xFFFFFFFFu ? 0x7FFFu : k0 >> C::IDX_BITS;
+                const uint32_t o1 = k1 == 0xFFFFFFFFu ? 0x7FFFu : k1 >> C::IDX_BITS;
+                const uint32_t s0 = __shfl_sync(0xffffffffu, gw[(2 * i) / 32], (2 * i) % 32);
+                const uint32_t s1 = __shfl_sync(0xffffffffu, gw[(2 * i + 1) / 32], (2 * i + 1) % 32);
+                const uint32_t t0 = min(o0, s0 ? 0xFFFFu - s0 + 1u : 0x7FFFu);
+                const uint32_t t1 = min(o1, s1 ? 0xFFFFu - s1 + 1u : 0x7FFFu);
+                const uint32_t lo = qb + 2 * i < a.nq ? t0 : 0u, hi = qb + 2 * i + 1 < a.nq ? t1 : 0u;
+                thrp[i] = lo | (hi << 16);
+            }
+        }
+        // fast test: bit 15 / 31 of (p | 0x80008000) - thr clear <=> that half is a candidate
+        uint32_t all = 0xFFFFFFFFu;
+#pragma unroll
+        for (int i = 0; i < NR; ++i) all &= (p[i] | 0x80008000u) - thrp[i];
+        if (!__any_sync(0xffffffffu, (all & 0x80008000u) != 0x80008000u)) continue;
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+            const uint32_t dd = (p[i] | 0x80008000u) - thrp[i];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint32_t cand = __ballot_sync(0xffffffffu, !(dd & (0x8000u << (16 * h))));
+                if (!cand) continue;
+                const int q = 2 * i + h;
+                uint32_t* L = lst + q * 32;
+                const uint32_t key = (((p[i] >> (16 * h)) & 0xFFFFu) << C::IDX_BITS) | (uint32_t)vl;
+                uint32_t kth = 0;
+                while (cand) {
+                    const int src = __ffs(cand) - 1;
+                    cand &= cand - 1;
+                    const uint32_t c = __shfl_sync(0xffffffffu, key, src);
+                    const uint32_t cur = L[lane];
+                    kth = __shfl_sync(0xffffffffu, cur, k - 1);
+                    if (c >= kth) continue;
+                    const uint32_t prev = __shfl_up_sync(0xffffffffu, cur, 1);
+                    const int pos = __popc(__ballot_sync(0xffffffffu, lane < k && cur < c));
+                    const uint32_t nw = lane == pos ? c : (lane > pos ? prev : cur);
+                    __syncwarp();
+                    if (lane < k) L[lane] = nw;
+                    __syncwarp();
+                    kth = __shfl_sync(0xffffffffu, nw, k - 1);
+                }
+                if (kth != 0xFFFFFFFFu) {
+                    const uint32_t okv = kth >> C::IDX_BITS;
+                    const uint32_t old = (thrp[i] >> (16 * h)) & 0xFFFFu;
+                    if (okv < old) {
+                        thrp[i] = (thrp[i] & ~(0xFFFFu << (16 * h))) | (okv << (16 * h));
+                        if (lane == 0 && qb + q < a.nq)
+                            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gthr_inv + qb + q),
+                                         "r"(0xFFFFu - okv)
+                                         : "memory");
+                    }
+                }
+            }
+        }
+    }
+    __syncwarp();
+    // lists -> part_keys[((part * 2 + rank) * 4 + quad)][query][k]
+    const int64_t li = ((int64_t)part * 2 + rank) * 4 + quad;
+    for (int q = 0; q < QW; ++q) {
+        if (qb + q >= a.nq) break;
+        if (lane < k) {
+            const uint32_t key = lst[q * 32 + lane];
+            uint64_t out = ~0ull;
+            if (key != 0xFFFFFFFFu) {
+                const uint32_t kvp = key >> C::IDX_BITS;
+                const uint32_t kv64 = kDot ? 0xFFFFu - (C::KVMAX - kvp) : kvp;
+                out = make_key(kv64, (uint64_t)(index_base + vbeg + (key & ((1u << C::IDX_BITS) - 1u))));
+            }
+            part_keys[(li * a.nq + qb + q) * k + lane] = out;
+        }
+    }
+}
+
+template <int M, bool kDot, int KMAX, int kOut = 0, bool kGroup = false, int kNQ = 0>
 __global__ void __launch_bounds__(kThreads, 1)
 topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, uint64_t* __restrict__ part_keys,
                uint32_t* __restrict__ gthr_inv, int xmode, FullOut fo, const __grid_constant__ CUtensorMap omap) {
 #ifndef BOLT_XMODE
     xmode = 0;  // diagnostic stage switches exist only in libbolt_x.so (tools/)
 #endif
-    using C = Cfg<M, (kOut != 0)>;
+    using C = Cfg<M, (kOut == 1 || kOut == 2), (kOut == 3 ? kNQ / 2 : kQM),
+                  (kOut == 3 ? kEpiWarps * (kNQ / 2) * 32 * 4 : 0)>;
     constexpr int S = C::STAGES;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sA = smem;
@@ -367,7 +545,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
     const int unit = blockIdx.x >> 1;
     const int tq = unit % tiles_q;
     const int part = unit / tiles_q;
-    const int64_t q0 = (int64_t)tq * 2 * kQM + rank * kQM;  // this CTA's queries
+    const int64_t q0 = (int64_t)tq * 2 * C::QR + rank * C::QR;  // this CTA's queries
     const int64_t vbeg = (int64_t)part * vpp;
     const int64_t vend = min64(a.n, vbeg + vpp);
     const int ntiles = vend > vbeg ? (int)ceil_div(vend - vbeg, C::N) : 0;
@@ -399,11 +577,11 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
         // ------------------------------------------------------ producers
         const int t = threadIdx.x - kEpilogue;
         // A: this CTA's 128 queries, 16-byte unit (c, q) -> c*(128*16) + (q/8)*128 + (q%8)*16
-        for (int u = t; u < kQM * M; u += kProducers) {
-            const int c = u / kQM, q = u % kQM;
+        for (int u = t; u < C::QR * M; u += kProducers) {
+            const int c = u / C::QR, q = u % C::QR;
             uint4 v = make_uint4(0, 0, 0, 0);
             if (q0 + q < a.nq) v = __ldg(reinterpret_cast<const uint4*>(a.qluts + ((q0 + q) * M + c) * kK));
-            *reinterpret_cast<uint4*>(sA + c * (kQM * 16) + (q >> 3) * 128 + (q & 7) * 16) = v;
+            *reinterpret_cast<uint4*>(sA + c * (C::QR * 16) + (q >> 3) * 128 + (q & 7) * 16) = v;
         }
         // Thread t expands vector v = t of each tile: its M code words (the
         // same for the 8 vectors of a layout-v1 group, one broadcast load)
@@ -480,6 +658,10 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             }
         }
     } else if (warp < kEpiWarps) {
+      if constexpr (kOut == 3) {
+        epilogue_swapped<C, kDot, kNQ>(a, k, index_base, vbeg, vend, ntiles, part, tq, rank, warp, lane, tmem, tfull,
+                                       tempty, scratch_all, part_keys, gthr_inv, xmode);
+      } else {
         // ------------------------------------------------------- epilogue
         const int quad = warp & 3;                 // TMEM lanes 32*quad .. (warp % 4 rule)
         const int half = warp >> 2;                // column half of the tile
@@ -748,6 +930,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                 }
             }
         }
+      }
     } else if (warp == kMmaWarp && rank == 0) {
         // ------------------------------------------- MMA issuer (leader CTA)
         if (lane == 0) {
@@ -770,12 +953,14 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
 #pragma unroll
                 for (int ks = 0; ks < C::KSTEPS; ++ks) {
                     // K step ks covers 16-byte chunks 2ks, 2ks+1 (same offsets in the peer CTA)
-                    const uint64_t ad = smem_desc(a_base + 2 * ks * (kQM * 16), kQM * 16, 128);
+                    const uint64_t ad = smem_desc(a_base + 2 * ks * (C::QR * 16), C::QR * 16, 128);
                     const uint64_t bd = smem_desc(bs + 2 * ks * (C::NH * 16), C::NH * 16, 128);
                     // top-k: D[query][vector] (A = tables); full output: the roles swap,
                     // D[vector][query] (A = one-hot), so that an epilogue thread owns
                     // consecutive queries of one output row
                     if (kOut == 0) mma_i8_pair(tmem + (uint32_t)(d * C::N), ad, bd, C::IDESC, ks > 0 ? 1u : 0u);
+                    else if (kOut == 3)
+                        mma_i8_pair(tmem + (uint32_t)(d * kNQ), bd, ad, C::IDESC_SW, ks > 0 ? 1u : 0u);
                     else mma_i8_pair(tmem + (uint32_t)(d * C::N), bd, ad, C::IDESC, ks > 0 ? 1u : 0u);
                 }
                 mma_commit_pair(&empty[s]);
@@ -796,16 +981,17 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
     }
 }
 
-template <int M, bool kDot, int KMAX, int kOut = 0, bool kGroup = false>
+template <int M, bool kDot, int KMAX, int kOut = 0, bool kGroup = false, int kNQ = 0>
 cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, uint64_t* part_keys,
                       uint32_t* gthr, cudaStream_t s, FullOut fo = FullOut{},
                       const CUtensorMap& omap = CUtensorMap{}) {
-    using C = Cfg<M, (kOut != 0)>;
-    const int tiles_q = (int)ceil_div(a.nq, 2 * kQM);
+    using C = Cfg<M, (kOut == 1 || kOut == 2), (kOut == 3 ? kNQ / 2 : kQM),
+                  (kOut == 3 ? kEpiWarps * (kNQ / 2) * 32 * 4 : 0)>;
+    const int tiles_q = (int)ceil_div(a.nq, 2 * C::QR);
     // full output with TMA stores: partitions of whole 256-vector tiles, so that
     // a tile's 256 rows never reach into the next partition
     const int64_t vpp = fo.tma ? ceil_div(ceil_div(a.n, rparts), C::N) * C::N : ceil_div(ceil_div(a.n, rparts), 8) * 8;
-    auto kern = topk_tc_kernel<M, kDot, KMAX, kOut, kGroup>;
+    auto kern = topk_tc_kernel<M, kDot, KMAX, kOut, kGroup, kNQ>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(2 * tiles_q * rparts));
@@ -824,7 +1010,10 @@ cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, 
     if (const char* x = getenv("BOLT_TC_XMODE")) xmode = atoi(x);
 #endif
     // shared thresholds: [nq] k-th-value words, then (8 B aligned) [nq][2] half-list words
-    if (kOut == 0 && kGroup) {  // large k: [nq][4] group words instead
+    if (kOut == 3) {  // swapped top-k: [nq] k-th-value words
+        cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)a.nq * sizeof(uint32_t), s);
+        if (e != cudaSuccess) return e;
+    } else if (kOut == 0 && kGroup) {  // large k: [nq][4] group words instead
         cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)a.nq * 4 * sizeof(uint32_t), s);
         if (e != cudaSuccess) return e;
     } else if (kOut == 0 && !(xmode & 16)) {  // diagnostic 16: keep caller-prefilled shared thresholds
@@ -939,6 +1128,53 @@ int topk_tc_parts(int64_t n, int m, int64_t nq, int k, int num_sms) {
     int rparts = choose_parts(tiles_q, ceil_div(n, 8), num_sms / 2, (int64_t)256 * 16 / 8);
     rparts = (int)max64(rparts, ceil_div(n, max_range - 8));
     return 2 * rparts;
+}
+
+namespace tc {
+
+// Swapped top-k (kOut = 3): small query batches, vectors on the MMA's M side.
+template <int M, int kNQ>
+cudaError_t launch_sw_q(const ScanArgs& a, int k, int metric, int64_t index_base, int rparts, uint64_t* part_keys,
+                        uint32_t* gthr, cudaStream_t s) {
+    return metric == BOLT_DOT ? launch_mk<M, true, 4, 3, false, kNQ>(a, k, index_base, rparts, part_keys, gthr, s)
+                              : launch_mk<M, false, 4, 3, false, kNQ>(a, k, index_base, rparts, part_keys, gthr, s);
+}
+template <int M>
+cudaError_t launch_sw_m(const ScanArgs& a, int k, int metric, int64_t index_base, int rparts, uint64_t* part_keys,
+                        uint32_t* gthr, cudaStream_t s) {
+    if (a.nq <= 32) return launch_sw_q<M, 32>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+    if (a.nq <= 64) return launch_sw_q<M, 64>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+    return launch_sw_q<M, 128>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+}
+
+}  // namespace tc
+
+int topk_tcs_supported(int64_t n, int m, int64_t nq, int k) {
+    return n >= 1 && nq >= 1 && nq <= 128 && k >= 1 && k <= 32 && (m == 8 || m == 16 || m == 32);
+}
+
+// 8 lists per query per row partition (2 CTAs x 4 quads); one wave of pairs
+// or more, each partition within the local index range
+int topk_tcs_parts(int64_t n, int m, int64_t nq, int k, int num_sms) {
+    (void)nq;
+    (void)k;
+    const int64_t max_range = m == 8 ? tc::Cfg<8>::MAX_RANGE : (m == 16 ? tc::Cfg<16>::MAX_RANGE : tc::Cfg<32>::MAX_RANGE);
+    int rparts = choose_parts(1, ceil_div(n, 8), num_sms / 2, (int64_t)256 * 16 / 8);
+    rparts = (int)max64(rparts, ceil_div(n, max_range - 8));
+    return 8 * rparts;
+}
+
+// part_keys: parts*nq*k keys followed by nq u32 shared thresholds
+cudaError_t launch_topk_tcs(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
+                            uint64_t* part_keys, cudaStream_t s) {
+    uint32_t* gthr = reinterpret_cast<uint32_t*>(part_keys + (size_t)parts * a.nq * k);
+    const int rparts = parts / 8;
+    switch (a.m) {
+        case 8: return tc::launch_sw_m<8>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+        case 16: return tc::launch_sw_m<16>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+        case 32: return tc::launch_sw_m<32>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 // part_keys holds parts*nq*k keys followed by nq u32 shared thresholds.

@@ -473,6 +473,42 @@ def test_c5_full_size_sampled(bolt, orc):
     np.testing.assert_array_equal(keys[qs], orc.topk(gcodes, qlh, cfg5.k, 0))
 
 
+# ------------------------------- swapped tcgen05 top-k (small query batches)
+TCS_SHAPES = [(3000, 16, 1, 10), (70_000, 16, 24, 10), (5003, 8, 33, 32), (20_000, 32, 64, 5), (9000, 16, 100, 1),
+              (130_001, 16, 128, 16), (257, 8, 65, 20), (1, 16, 3, 4)]
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+@pytest.mark.parametrize("n,m,nq,k", TCS_SHAPES)
+def test_topk_tcs_bit_exact(bolt, orc, metric, n, m, nq, k):
+    """Vectors on the MMA's M side, queries on N (32/64/128): bit-exact keys
+    for ragged n (partial tiles, several partitions), nq inside a query tile,
+    k up to 32, both metrics."""
+    flat = G.random_codes(n, m, 500 + n)
+    ql = G.random_qluts(nq, m, 501 + nq)
+    got = host(bolt.topk(pack_on_gpu(bolt, flat), n, dev(ql), k, metric, index_base=5, variant=bolt.VARIANT_TCS))
+    np.testing.assert_array_equal(got, orc.topk(flat, ql, k, metric, index_base=5))
+
+
+def test_topk_tcs_ties_and_model_tables(bolt, orc):
+    n, m, nq = 40_000, 16, 20
+    flat = G.random_codes(n, m, 77)
+    for hi in (2, 16):
+        ql = G.random_qluts(nq, m, 78 + hi, hi=hi)
+        for metric in (0, 1):
+            got = host(bolt.topk(pack_on_gpu(bolt, flat), n, dev(ql), 32, metric, variant=bolt.VARIANT_TCS))
+            np.testing.assert_array_equal(got, orc.topk(flat, ql, 32, metric))
+    cfg = G.CONFIGS["c2"]
+    X = G.database(cfg, 50_000)
+    train = G.training(cfg, 4000)
+    C = orc.fit(train, cfg.m, G.kmeans_init_all(cfg, len(train)), 2)
+    a, b, _ = orc.fit_quantizer(G.calibration(cfg, train)[:100], C, 0)
+    codes = bolt.encode(dev(X), dev(C))
+    ql = bolt.build_quantized_luts(dev(G.queries(cfg, 40)), dev(C), 0, float(a), dev(b))
+    got = host(bolt.topk(codes, 50_000, ql, 10, 0, variant=bolt.VARIANT_TCS))
+    np.testing.assert_array_equal(got, orc.topk(orc.unpack_v1(host(codes), 50_000, cfg.m), host(ql), 10, 0))
+
+
 # --------------------------------------------- Bolt No Quantize (f3, O13/O14)
 F32_SHAPES = [(1, 1, 1), (300, 8, 5), (1001, 16, 33), (4099, 32, 64), (257, 64, 7), (5000, 5, 40)]
 

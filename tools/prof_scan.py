@@ -42,7 +42,7 @@ else:
     codes = bolt.pack_codes(torch.from_numpy(G.random_codes(a.n, a.m, 1)).to(dev))
     ql = torch.from_numpy(G.random_qluts(a.nq, a.m, 2)).to(dev)
     metric = 0
-v = {"prmt": bolt.VARIANT_PRMT, "tc": bolt.VARIANT_TC, "auto": bolt.VARIANT_AUTO}[a.variant]
+v = {"prmt": bolt.VARIANT_PRMT, "tc": bolt.VARIANT_TC, "tcs": bolt.VARIANT_TCS, "auto": bolt.VARIANT_AUTO}[a.variant]
 if a.what == "encode":
     X = torch.from_numpy(G.database(G.CONFIGS["c2"], a.n)).to(dev)
     C = torch.from_numpy(G.random_floats((a.m, 16, 128 // a.m), 3, 50.0) + 100).to(dev)
