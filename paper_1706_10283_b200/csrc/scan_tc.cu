@@ -576,13 +576,20 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
     if (warp >= kEpiWarps && warp < kMmaWarp) {
         // ------------------------------------------------------ producers
         const int t = threadIdx.x - kEpilogue;
-        // A: this CTA's 128 queries, 16-byte unit (c, q) -> c*(128*16) + (q/8)*128 + (q%8)*16
+        // A: this CTA's queries, 16-byte unit (c, q) -> c*(QR*16) + (q/8)*128 + (q%8)*16,
+        // as asynchronous copies (LDGSTS) issued back to back -- a dependent
+        // load/store loop took ~10 us per unit for 64 KB of tables -- with
+        // zero fill past nq; completed below before the first full arrive
         for (int u = t; u < C::QR * M; u += kProducers) {
             const int c = u / C::QR, q = u % C::QR;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (q0 + q < a.nq) v = __ldg(reinterpret_cast<const uint4*>(a.qluts + ((q0 + q) * M + c) * kK));
-            *reinterpret_cast<uint4*>(sA + c * (C::QR * 16) + (q >> 3) * 128 + (q & 7) * 16) = v;
+            const bool ok = q0 + q < a.nq;
+            const uint8_t* src = a.qluts + ((ok ? q0 + q : 0) * M + c) * kK;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                             smem_u32(sA + c * (C::QR * 16) + (q >> 3) * 128 + (q & 7) * 16)),
+                         "l"(src), "r"(ok ? 16 : 0)
+                         : "memory");
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         // Thread t expands vector v = t of each tile: its M code words (the
         // same for the 8 vectors of a layout-v1 group, one broadcast load)
         // are fetched from global memory a tile ahead, so no producer barrier
