@@ -821,6 +821,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                     }
                     __syncwarp();
                 }
+                if (lane == 0) BOLT_TRACE(tile, 27 + warp);
                 continue;
             }
             // shared threshold: use the value fetched one tile ago, prefetch the next
@@ -1090,7 +1091,10 @@ cudaError_t launch_scan_tc(const ScanArgs& a, uint16_t* out16, float* out32, int
     // query tables) would dominate short ones
     const int64_t tiles_q = ceil_div(a.nq, 2 * tc::kQM);
     const int64_t pairs = sms / 2;
-    const int rparts = (int)max64(1, min64(pairs / max64(tiles_q, 1), ceil_div(a.groups, 32)));
+    int rparts = (int)max64(1, min64(pairs / max64(tiles_q, 1), ceil_div(a.groups, 32)));
+#ifdef BOLT_XMODE
+    if (const char* e = getenv("BOLT_TC_RPARTS")) rparts = atoi(e);  // diagnostic sweeps (tools/)
+#endif
     void* out = out32 ? static_cast<void*>(out32) : static_cast<void*>(out16);
     const int esz = out32 ? 4 : 2;
     const int vec = (reinterpret_cast<uintptr_t>(out) % 16 == 0) && ((ldo * esz) % 16 == 0);

@@ -411,6 +411,54 @@ def test_c2_full_size_sampled(bolt, orc):
     np.testing.assert_array_equal(keys[qs], orc.topk(gcodes, qlh[qs], cfg.k, 0))
 
 
+@pytest.mark.slow
+def test_c3_full_size_sampled(bolt, orc):
+    """BASELINE c3 (N=1M, J=512, M=32, Q=1k, dot product, top-10 MIPS) in the
+    bench launch configuration: 16 sampled queries checked by the oracle over
+    the full GPU code set; 10k sampled rows re-encoded by the oracle."""
+    cfg = G.CONFIGS["c3"]
+    X = G.database(cfg)
+    train = G.training(cfg, 10_000)
+    C = orc.fit(train, cfg.m, G.kmeans_init_all(cfg, len(train)), 3)
+    a, b, _ = orc.fit_quantizer(G.calibration(cfg, train)[:200], C, 1)
+    codes = bolt.encode(dev(X), dev(C))
+    ql = bolt.build_quantized_luts(dev(G.queries(cfg)), dev(C), 1, float(a), dev(b))
+    assert bolt.topk_plan(cfg.n, cfg.m, cfg.nq, cfg.k)[0] == "tc"
+    keys = host(bolt.topk(codes, cfg.n, ql, cfg.k, 1))
+    gcodes = orc.unpack_v1(host(codes), cfg.n, cfg.m)
+    rows = np.random.default_rng(3).choice(cfg.n, 10_000, replace=False)
+    ref_codes, gap = orc.encode(X[rows], C, with_gap=True)
+    d = gcodes[rows] != ref_codes
+    assert (d <= (gap < 1e-5)).all() and d.sum() <= NEAR_TIE_CAP * d.size
+    qs = np.random.default_rng(4).choice(cfg.nq, 16, replace=False)
+    np.testing.assert_array_equal(keys[qs], orc.topk(gcodes, host(ql)[qs], cfg.k, 1))
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled(bolt, orc):
+    """BASELINE c4 (A 100k x 256 encoded, B 256 x 1024 as queries, fused
+    dequantised fp32 output [100k][1024]) in the bench launch configuration
+    (tcgen05 full output, TMA stores): the whole u16 sum matrix is exact and
+    sampled rows of the fp32 output match the oracle's dequantisation."""
+    cfg = G.CONFIGS["c4"]
+    X = G.database(cfg)
+    Q = G.queries(cfg)
+    C = orc.fit(X[:20_000], cfg.m, G.kmeans_init_all(cfg, 20_000), 3)
+    a, b, _ = orc.fit_quantizer(G.calibration(cfg, X)[:200], C, 1)
+    codes = bolt.encode(dev(X), dev(C))
+    ql = bolt.build_quantized_luts(dev(Q), dev(C), 1, float(a), dev(b))
+    gcodes = orc.unpack_v1(host(codes), cfg.n, cfg.m)
+    qlh = host(ql)
+    acc = host(bolt.scan(codes, cfg.n, ql))
+    np.testing.assert_array_equal(acc, orc.scan(gcodes, qlh))
+    bsum = float(np.sum(b.astype(np.float64)))
+    out = host(bolt.scan_dequant(codes, cfg.n, ql, float(a), np.float32(bsum)))
+    rows = np.random.default_rng(5).choice(cfg.n, 2000, replace=False)
+    ref = orc.dequant(acc[rows], float(a), b)
+    tol = 2.0**-21 * (np.abs(acc[rows] / np.float64(a)) + abs(bsum))
+    assert (np.abs(out[rows] - ref) <= tol).all()
+
+
 # ------------------------------------- c5 / sweep: device-generated database
 def test_c5_device_rows_sampled(bolt, orc):
     """c5's rows come from the GPU generator (synth/gen_gpu.cu); a slice far
