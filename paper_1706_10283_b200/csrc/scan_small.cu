@@ -66,7 +66,7 @@ __device__ __forceinline__ void group_sums(const uint4 (&w)[M / 4], const uint4*
             const uint32_t s0 = (t & 3) == 0 ? wv.x : (t & 3) == 1 ? wv.y : (t & 3) == 2 ? wv.z : wv.w;
             const uint32_t x0 = s0 ^ 0x88888888u;
             const uint32_t s1 = imul_hi(s0, hi16);  // s0 >> 16 on the FMA pipe
-            const uint32_t x1 = imul_hi(x0, hi16);
+            const uint32_t x1 = s1 ^ 0x8888u;        // (s0 ^ 0x88888888) >> 16 on the ALU (balances the pipes)
 #pragma unroll
             for (int q = 0; q < QT; ++q) {
                 const uint4 lo = tab[2 * (q * M + t)];
