@@ -151,7 +151,8 @@ def workload(args, rank):
     return cfg, n, nq
 
 
-def cpu_baseline_sample(cfg, X, Q, C, a, b, metric, k, budget_s=20.0, dequant=False):
+def cpu_baseline_sample(cfg, X, Q, C, a, b, metric, k, budget_s=20.0, dequant=False, noquant=False,
+                        with_encode=True):
     """The fp64 oracle, as it stands, on the host cores: encode of the full
     database shard, tables of all queries, and the scan + top-k for a sample
     of queries over the full database; the scan time is scaled to all
@@ -163,27 +164,31 @@ def cpu_baseline_sample(cfg, X, Q, C, a, b, metric, k, budget_s=20.0, dequant=Fa
     flat = oracle.encode(X, C)
     t_enc = time.perf_counter() - t0
     t0 = time.perf_counter()
-    ql = oracle.quantize(oracle.luts(Q, C, metric), a, b)
+    D = oracle.luts(Q, C, metric)
+    ql = D.astype(np.float32) if noquant else oracle.quantize(D, a, b)
     t_lut = time.perf_counter() - t0
     # size the scan sample to the remaining budget (at least 8 queries)
     def scan_part(qn):
-        if k > 0:
+        if noquant:
+            oracle.topk_f32(flat, ql[:qn], k, metric)
+        elif k > 0:
             oracle.topk(flat, ql[:qn], k, metric)
         else:
             acc = oracle.scan(flat, ql[:qn])
             if dequant:
                 oracle.dequant(acc, a, b)
 
+    q8 = min(8, nq)
     t0 = time.perf_counter()
-    scan_part(8)
+    scan_part(q8)
     t8 = time.perf_counter() - t0
-    qs = int(max(8, min(nq, 8 * max(1.0, (budget_s - t_enc - t_lut - t8) / max(t8, 1e-3)))))
-    qs = min(qs, 1024)
+    qs = int(max(q8, min(nq, q8 * max(1.0, (budget_s - t_enc - t_lut - t8) / max(t8, 1e-3)))))
+    qs = min(qs, 1024, nq)
     t0 = time.perf_counter()
     scan_part(qs)
     t_scan = time.perf_counter() - t0
-    t_full = t_enc + t_lut + t_scan * (nq / qs)
-    desc = (f"oracle encode of all {n} rows ({t_enc:.2f} s) + fp64 tables of all {nq} queries "
+    t_full = (t_enc if with_encode else 0.0) + t_lut + t_scan * (nq / qs)
+    desc = (f"oracle encode of all {n} rows ({t_enc:.2f} s{'' if with_encode else ', not counted: the step has no encode'}) + fp64 tables of all {nq} queries "
             f"({t_lut:.2f} s) + scan{f'/top-{k}' if k else (' + dequant' if dequant else '')} of {qs} queries "
             f"over all rows ({t_scan:.2f} s), "
             f"scan scaled x{nq / qs:.1f} to {nq} queries")
@@ -822,9 +827,16 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import oracle
-    cfg, n, nq = workload(args, rank)
-    metric, k = cfg.metrics[0], cfg.k
-    X = G.database(cfg, n)
+    # sweep: c5's database at Q = 1; c2nq: c2 with the fp32 tables (O13/O14)
+    name = {"sweep": "c5", "c2nq": "c2"}.get(args.config, args.config)
+    cfg = G.CONFIGS[name]
+    n, nq = args.n or cfg.n, args.nq or (1 if args.config == "sweep" else cfg.nq)
+    metric, k = cfg.metrics[0], (10 if args.config == "sweep" else cfg.k)
+    # the oracle's cost is linear in the rows, so its distances/s on a row
+    # sample of the same distribution is the full-size rate: at most 1M rows
+    # (c5's 1e8-row database never exists on the host)
+    n_s = min(n, 1_000_000)
+    X = G.database(cfg, n_s)
     Q = G.queries(cfg, nq)
     train = G.training(cfg, 20_000)
     C = oracle.fit(train, cfg.m, G.kmeans_init_all(cfg, len(train)), cfg.kmeans_iters)
@@ -833,7 +845,11 @@ def run_reference(args):
     vals = []
     desc = cores = None
     for i in range(args.warmup + args.steps):
-        v, cores, desc = cpu_baseline_sample(cfg, X, Q, C, a, b, metric, k, budget_s=budget)
+        v, cores, desc = cpu_baseline_sample(cfg, X, Q, C, a, b, metric, k, budget_s=budget,
+                                             noquant=args.config == "c2nq",
+                                             with_encode=args.config not in ("c5", "sweep"))
+        if n_s < n:
+            desc += f"; rows: a {n_s}-row sample of the {n}-row database (same mixture), rate per distance"
         if i >= args.warmup:
             vals.append(v)
     value = statistics.mean(vals)
