@@ -98,12 +98,14 @@ constexpr int kScratchStrideFull = 32;
 // QROWS: query rows of the table buffer per CTA (kQM, or kNQ/2 in the
 // swapped top-k); LIST_BYTES: the swapped top-k's per-warp lists (else the
 // scratch rows of the other modes)
-template <int M, bool kFull = false, int QROWS = kQM, int LIST_BYTES = 0>
+// PAIR: cta_group::2 (a CTA pair shares each 256-vector tile, 128 queries per
+// CTA) or cta_group::1 (one CTA, 128 queries, expands all 256 vectors)
+template <int M, bool kFull = false, int QROWS = kQM, int LIST_BYTES = 0, bool PAIR = true>
 struct Cfg {
     static constexpr int SCRATCH_STRIDE = kFull ? kScratchStrideFull : kScratchStrideTopk;
     static constexpr int K = 16 * M;                      // bytes per row
-    static constexpr int N = 256;                         // vectors per MMA tile (pair)
-    static constexpr int NH = N / 2;                      // vectors per CTA (its half of B)
+    static constexpr int N = 256;                         // vectors per MMA tile
+    static constexpr int NH = PAIR ? N / 2 : N;           // vectors whose one-hot this CTA holds
     static constexpr int QR = QROWS;
     static constexpr int A_BYTES = QROWS * K;
     static constexpr int B_BYTES = NH * K;                // one stage of this CTA's half of B
@@ -124,7 +126,7 @@ struct Cfg {
     static constexpr int SMEM = BAR_OFF + 256;
     // instruction descriptor: D s32 (bits 4-5 = 2), A/B u8 (format 0), K-major,
     // N >> 3 at bit 17, M >> 4 at bit 24 (M = 256 for the pair)
-    static constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+    static constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)((PAIR ? 256 : 128) >> 4) << 24);
     // swapped top-k: M = 256 vectors (A = one-hot), N = 2 QROWS queries (B = tables)
     static constexpr uint32_t IDESC_SW = (2u << 4) | ((uint32_t)((2 * QROWS) >> 3) << 17) |
                                          ((uint32_t)(256 >> 4) << 24);
@@ -221,6 +223,18 @@ __device__ __forceinline__ void mma_i8_pair(uint32_t d_tmem, uint64_t a, uint64_
         "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
+}
+__device__ __forceinline__ void mma_i8_single(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_single(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
 }
 // commit the leader's MMAs to the barrier at the same offset in both CTAs
 __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
@@ -518,7 +532,7 @@ __device__ __forceinline__ void epilogue_swapped(const ScanArgs& a, int k, int64
     }
 }
 
-template <int M, bool kDot, int KMAX, int kOut = 0, bool kGroup = false, int kNQ = 0>
+template <int M, bool kDot, int KMAX, int kOut = 0, bool kGroup = false, int kNQ = 0, bool kPairT = true>
 __global__ void __launch_bounds__(kThreads, 1)
 topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, uint64_t* __restrict__ part_keys,
                uint32_t* __restrict__ gthr_inv, int xmode, FullOut fo, const __grid_constant__ CUtensorMap omap) {
@@ -526,7 +540,8 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
     xmode = 0;  // diagnostic stage switches exist only in libbolt_x.so (tools/)
 #endif
     using C = Cfg<M, (kOut == 1 || kOut == 2), (kOut == 3 ? kNQ / 2 : kQM),
-                  (kOut == 3 ? kEpiWarps * (kNQ / 2) * 32 * 4 : 0)>;
+                  (kOut == 3 ? kEpiWarps * (kNQ / 2) * 32 * 4 : 0), kPairT>;
+    static_assert(kPairT || kOut == 0, "single-CTA tiles only for the top-k");
     constexpr int S = C::STAGES;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sA = smem;
@@ -541,34 +556,44 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
-    const int unit = blockIdx.x >> 1;
+    const uint32_t rank = kPairT ? cluster_rank() : 0u;
+    const int unit = kPairT ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     const int tq = unit % tiles_q;
     const int part = unit / tiles_q;
-    const int64_t q0 = (int64_t)tq * 2 * C::QR + rank * C::QR;  // this CTA's queries
+    const int64_t q0 = (int64_t)tq * (kPairT ? 2 : 1) * C::QR + rank * C::QR;  // this CTA's queries
     const int64_t vbeg = (int64_t)part * vpp;
     const int64_t vend = min64(a.n, vbeg + vpp);
     const int ntiles = vend > vbeg ? (int)ceil_div(vend - vbeg, C::N) : 0;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
-            mbar_init(&full[i], 2 * kProdWarps);  // one arrive per producer warp of both CTAs
+            mbar_init(&full[i], (kPairT ? 2 : 1) * kProdWarps);  // one arrive per producer warp of both CTAs
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 2 * kEpiWarps);  // one arrive per epilogue warp of both CTAs
+            mbar_init(&tempty[i], (kPairT ? 2 : 1) * kEpiWarps);  // one arrive per epilogue warp of both CTAs
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kMmaWarp) {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"((uint32_t)C::TMEM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        if constexpr (kPairT) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"((uint32_t)C::TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"((uint32_t)C::TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     tc_fence_before();
-    cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+    if constexpr (kPairT) cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const long long tk0 = BOLT_CLOCK();
@@ -594,49 +619,56 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
         // same for the 8 vectors of a layout-v1 group, one broadcast load)
         // are fetched from global memory a tile ahead, so no producer barrier
         // is needed; each warp arrives on the stage's full barrier on its own.
-        static_assert(C::NH == kProducers, "one producer thread per vector");
+        constexpr int VPT = C::NH / kProducers;     // vectors per producer thread (1 pair, 2 single)
+        static_assert(VPT * kProducers == C::NH, "whole vectors per producer thread");
         constexpr int MH = M;                       // codebooks per producer thread
-        constexpr int NW4 = MH / 4;                 // uint4 loads per thread
-        const int v = t;
+        constexpr int NW4 = MH / 4;                 // uint4 loads per vector
         constexpr int ch = 0;
-        const uint32_t sh = (v & 7) * 4;
-        auto load_words = [&](int tile, uint4 (&w)[NW4]) {
-            const int64_t g = (vbeg + (int64_t)tile * C::N + rank * C::NH + v) >> 3;
+        const uint32_t sh = (t & 7) * 4;            // kProducers % 8 == 0: the same for every vector of t
+        auto load_words = [&](int tile, uint4 (&w)[VPT][NW4]) {
 #pragma unroll
-            for (int i = 0; i < NW4; ++i)
-                w[i] = g < a.groups ? __ldg(reinterpret_cast<const uint4*>(a.codes + g * M + ch * MH) + i)
-                                    : make_uint4(0, 0, 0, 0);
+            for (int u = 0; u < VPT; ++u) {
+                const int64_t g = (vbeg + (int64_t)tile * C::N + rank * C::NH + t + u * kProducers) >> 3;
+#pragma unroll
+                for (int i = 0; i < NW4; ++i)
+                    w[u][i] = g < a.groups ? __ldg(reinterpret_cast<const uint4*>(a.codes + g * M + ch * MH) + i)
+                                           : make_uint4(0, 0, 0, 0);
+            }
         };
         // one tile of expansion: wait for the stage, write the one-hot rows,
         // publish them to the async proxy and arrive on the stage's full barrier
-        auto produce = [&](int tile, const uint4 (&cur)[NW4]) {
+        auto produce = [&](int tile, const uint4 (&cur)[VPT][NW4]) {
             const int s = tile % S;
             long long tw0 = BOLT_CLOCK();
             mbar_wait(&empty[s], ((tile / S) & 1) ^ 1);
             if (lane == 0) BOLT_TRACE(tile, 3 + t / 32);
             if (t == 0) BOLT_PROF_ADD(0, BOLT_CLOCK() - tw0);  // producer waits on empty
-            uint8_t* b = sB + s * C::B_BYTES + ch * MH * (C::NH * 16) + v * 16;
             const int64_t hb = vbeg + (int64_t)tile * C::N + rank * C::NH;  // first vector of this half
-            if (xmode & 2) {
-                // diagnostic: keep the stage's stale one-hot rows
-            } else if (hb + C::NH <= vend) {
 #pragma unroll
-                for (int i = 0; i < NW4; ++i) {
-                    const uint32_t ws[4] = {cur[i].x, cur[i].y, cur[i].z, cur[i].w};
+            for (int u = 0; u < VPT; ++u) {
+                const int v = t + u * kProducers;
+                uint8_t* b = sB + s * C::B_BYTES + ch * MH * (C::NH * 16) + v * 16;
+                if (xmode & 2) {
+                    // diagnostic: keep the stage's stale one-hot rows
+                } else if (hb + C::NH <= vend) {
 #pragma unroll
-                    for (int j = 0; j < 4 && 4 * i + j < MH; ++j)
-                        *reinterpret_cast<uint4*>(b + (4 * i + j) * (C::NH * 16)) =
-                            one_hot16_s(((ws[j] >> sh) & 0xFu) * 8u);
-                }
-            } else {  // last, partial tile: rows past the range are all-zero
-                const bool valid = hb + v < vend;
+                    for (int i = 0; i < NW4; ++i) {
+                        const uint32_t ws[4] = {cur[u][i].x, cur[u][i].y, cur[u][i].z, cur[u][i].w};
 #pragma unroll
-                for (int i = 0; i < NW4; ++i) {
-                    const uint32_t ws[4] = {cur[i].x, cur[i].y, cur[i].z, cur[i].w};
+                        for (int j = 0; j < 4 && 4 * i + j < MH; ++j)
+                            *reinterpret_cast<uint4*>(b + (4 * i + j) * (C::NH * 16)) =
+                                one_hot16_s(((ws[j] >> sh) & 0xFu) * 8u);
+                    }
+                } else {  // last, partial tile: rows past the range are all-zero
+                    const bool valid = hb + v < vend;
 #pragma unroll
-                    for (int j = 0; j < 4 && 4 * i + j < MH; ++j)
-                        *reinterpret_cast<uint4*>(b + (4 * i + j) * (C::NH * 16)) =
-                            one_hot16_s(valid ? ((ws[j] >> sh) & 0xFu) * 8u : 128u);
+                    for (int i = 0; i < NW4; ++i) {
+                        const uint32_t ws[4] = {cur[u][i].x, cur[u][i].y, cur[u][i].z, cur[u][i].w};
+#pragma unroll
+                        for (int j = 0; j < 4 && 4 * i + j < MH; ++j)
+                            *reinterpret_cast<uint4*>(b + (4 * i + j) * (C::NH * 16)) =
+                                one_hot16_s(valid ? ((ws[j] >> sh) & 0xFu) * 8u : 128u);
+                    }
                 }
             }
             fence_proxy_async();
@@ -649,8 +681,8 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
         };
         // code words prefetched kPrefetch tiles ahead (a register ring indexed
         // statically by unrolling the tile loop), issued after each arrive
-        constexpr int D = kPrefetch;
-        uint4 pre[D][NW4];
+        constexpr int D = VPT == 1 ? kPrefetch : 2;
+        uint4 pre[D][VPT][NW4];
 #pragma unroll
         for (int j = 0; j < D; ++j)
             if (j < ntiles) load_words(j, pre[j]);
@@ -966,13 +998,20 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                     // top-k: D[query][vector] (A = tables); full output: the roles swap,
                     // D[vector][query] (A = one-hot), so that an epilogue thread owns
                     // consecutive queries of one output row
-                    if (kOut == 0) mma_i8_pair(tmem + (uint32_t)(d * C::N), ad, bd, C::IDESC, ks > 0 ? 1u : 0u);
+                    if (kOut == 0 && !kPairT)
+                        mma_i8_single(tmem + (uint32_t)(d * C::N), ad, bd, C::IDESC, ks > 0 ? 1u : 0u);
+                    else if (kOut == 0) mma_i8_pair(tmem + (uint32_t)(d * C::N), ad, bd, C::IDESC, ks > 0 ? 1u : 0u);
                     else if (kOut == 3)
                         mma_i8_pair(tmem + (uint32_t)(d * kNQ), bd, ad, C::IDESC_SW, ks > 0 ? 1u : 0u);
                     else mma_i8_pair(tmem + (uint32_t)(d * C::N), bd, ad, C::IDESC, ks > 0 ? 1u : 0u);
                 }
-                mma_commit_pair(&empty[s]);
-                mma_commit_pair(&tfull[d]);
+                if constexpr (kPairT) {
+                    mma_commit_pair(&empty[s]);
+                    mma_commit_pair(&tfull[d]);
+                } else {
+                    mma_commit_single(&empty[s]);
+                    mma_commit_single(&tfull[d]);
+                }
                 BOLT_TRACE(tile, 2);
             }
         }
@@ -981,28 +1020,35 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
     if (threadIdx.x == 0) BOLT_PROF_ADD(6, BOLT_CLOCK() - tk0);   // CTA main-loop cycles
     if (threadIdx.x == 0) BOLT_PROF_ADD(7, 1);                    // CTAs
     tc_fence_before();
-    cluster_sync();  // all MMAs done and consumed in both CTAs
+    if constexpr (kPairT) cluster_sync();  // all MMAs done and consumed in both CTAs
+    else __syncthreads();
     if (warp == kMmaWarp) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS)
-                     : "memory");
+        if constexpr (kPairT)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                         "r"((uint32_t)C::TMEM_COLS)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                         "r"((uint32_t)C::TMEM_COLS)
+                         : "memory");
     }
 }
 
-template <int M, bool kDot, int KMAX, int kOut = 0, bool kGroup = false, int kNQ = 0>
+template <int M, bool kDot, int KMAX, int kOut = 0, bool kGroup = false, int kNQ = 0, bool kPairT = true>
 cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, uint64_t* part_keys,
                       uint32_t* gthr, cudaStream_t s, FullOut fo = FullOut{},
                       const CUtensorMap& omap = CUtensorMap{}) {
     using C = Cfg<M, (kOut == 1 || kOut == 2), (kOut == 3 ? kNQ / 2 : kQM),
-                  (kOut == 3 ? kEpiWarps * (kNQ / 2) * 32 * 4 : 0)>;
-    const int tiles_q = (int)ceil_div(a.nq, 2 * C::QR);
+                  (kOut == 3 ? kEpiWarps * (kNQ / 2) * 32 * 4 : 0), kPairT>;
+    const int tiles_q = (int)ceil_div(a.nq, (kPairT ? 2 : 1) * C::QR);
     // full output with TMA stores: partitions of whole 256-vector tiles, so that
     // a tile's 256 rows never reach into the next partition
     const int64_t vpp = fo.tma ? ceil_div(ceil_div(a.n, rparts), C::N) * C::N : ceil_div(ceil_div(a.n, rparts), 8) * 8;
-    auto kern = topk_tc_kernel<M, kDot, KMAX, kOut, kGroup, kNQ>;
+    auto kern = topk_tc_kernel<M, kDot, KMAX, kOut, kGroup, kNQ, kPairT>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(2 * tiles_q * rparts));
+    cfg.gridDim = dim3((unsigned)((kPairT ? 2 : 1) * tiles_q * rparts));
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = s;
@@ -1012,7 +1058,7 @@ cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, 
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = kPairT ? 1 : 0;  // single-CTA tiles: no cluster
     int xmode = 0;
 #ifdef BOLT_XMODE
     if (const char* x = getenv("BOLT_TC_XMODE")) xmode = atoi(x);
@@ -1056,25 +1102,47 @@ inline EncodeTiledFn encode_tiled() {
     return fn;
 }
 
-template <int M>
-cudaError_t launch_m(const ScanArgs& a, int k, int metric, int64_t index_base, int rparts, uint64_t* part_keys,
-                     uint32_t* gthr, cudaStream_t s) {
+template <int M, bool kPairT>
+cudaError_t launch_mp(const ScanArgs& a, int k, int metric, int64_t index_base, int rparts, uint64_t* part_keys,
+                      uint32_t* gthr, cudaStream_t s) {
     const bool dot = metric == BOLT_DOT;
     // register list capacity: smallest of {4, 12, 16, 32} >= k (bubble cost ~ 2 KMAX)
     if (k <= 4)
-        return dot ? launch_mk<M, true, 4>(a, k, index_base, rparts, part_keys, gthr, s)
-                   : launch_mk<M, false, 4>(a, k, index_base, rparts, part_keys, gthr, s);
+        return dot ? launch_mk<M, true, 4, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 4, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s);
     if (k <= 12)
-        return dot ? launch_mk<M, true, 12>(a, k, index_base, rparts, part_keys, gthr, s)
-                   : launch_mk<M, false, 12>(a, k, index_base, rparts, part_keys, gthr, s);
+        return dot ? launch_mk<M, true, 12, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 12, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s);
     if (k <= 16)
-        return dot ? launch_mk<M, true, 16>(a, k, index_base, rparts, part_keys, gthr, s)
-                   : launch_mk<M, false, 16>(a, k, index_base, rparts, part_keys, gthr, s);
-    if (a.noshare > 0)  // lists of 32 for k > 32: group-shared thresholds
-        return dot ? launch_mk<M, true, 32, 0, true>(a, k, index_base, rparts, part_keys, gthr, s)
-                   : launch_mk<M, false, 32, 0, true>(a, k, index_base, rparts, part_keys, gthr, s);
-    return dot ? launch_mk<M, true, 32>(a, k, index_base, rparts, part_keys, gthr, s)
-               : launch_mk<M, false, 32>(a, k, index_base, rparts, part_keys, gthr, s);
+        return dot ? launch_mk<M, true, 16, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 16, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s);
+    if constexpr (kPairT)
+        if (a.noshare > 0)  // lists of 32 for k > 32: group-shared thresholds
+            return dot ? launch_mk<M, true, 32, 0, true>(a, k, index_base, rparts, part_keys, gthr, s)
+                       : launch_mk<M, false, 32, 0, true>(a, k, index_base, rparts, part_keys, gthr, s);
+    return dot ? launch_mk<M, true, 32, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s)
+               : launch_mk<M, false, 32, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s);
+}
+
+// Single-CTA tiles (cta_group::1, 128 queries per CTA) for batches of at
+// most 128 queries: a 128-query pair tile would be half padding, and a
+// K = 32 step costs the same ~133 cycles per SM for 128 query rows either
+// way, so one CTA per 256-vector tile doubles the vectors per SM.
+// M <= 16 only: a 256-vector stage of M = 32 one-hot is 128 KB (no double buffer).
+inline bool tc_single(int64_t nq, int m, int k, int noshare) {
+#ifdef BOLT_XMODE
+    if (getenv("BOLT_TC_NO_SINGLE")) return false;  // diagnostic A/B (tools/)
+#endif
+    return nq <= kQM && m <= 16 && k <= 32 && noshare == 0;
+}
+
+template <int M>
+cudaError_t launch_m(const ScanArgs& a, int k, int metric, int64_t index_base, int rparts, uint64_t* part_keys,
+                     uint32_t* gthr, cudaStream_t s) {
+    if constexpr (M <= 16)
+        if (tc_single(a.nq, M, k, a.noshare))
+            return launch_mp<M, false>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+    return launch_mp<M, true>(a, k, metric, index_base, rparts, part_keys, gthr, s);
 }
 
 }  // namespace tc
@@ -1133,10 +1201,10 @@ int topk_tc_supported(int64_t n, int m, int64_t nq, int k) {
 // within the epilogue's local index bits.  Two partial lists per unit (the
 // two column-half epilogue warps).
 int topk_tc_parts(int64_t n, int m, int64_t nq, int k, int num_sms) {
-    (void)k;
-    const int64_t tiles_q = ceil_div(nq, 2 * tc::kQM);
+    const bool single = tc::tc_single(nq, m, k, k > 32 ? 1 : 0);  // k > 32: pair lists of 32 (api.cu)
+    const int64_t tiles_q = ceil_div(nq, (single ? 1 : 2) * tc::kQM);
     const int64_t max_range = m == 8 ? tc::Cfg<8>::MAX_RANGE : (m == 16 ? tc::Cfg<16>::MAX_RANGE : tc::Cfg<32>::MAX_RANGE);
-    int rparts = choose_parts(tiles_q, ceil_div(n, 8), num_sms / 2, (int64_t)256 * 16 / 8);
+    int rparts = choose_parts(tiles_q, ceil_div(n, 8), single ? num_sms : num_sms / 2, (int64_t)256 * 16 / 8);
     rparts = (int)max64(rparts, ceil_div(n, max_range - 8));
     return 2 * rparts;
 }
