@@ -246,6 +246,10 @@ TC_CASES = [
     (20000, 32, 64, 30, 256, 2**40),
     (20000, 16, 64, 32, 256, 2**40),
     (100000, 16, 300, 10, 256, 0),
+    # single-CTA 128-query tiles (nq <= 128, m <= 16, k <= 32)
+    (65537, 8, 128, 12, 8, 0),
+    (1_000_000, 16, 100, 10, 256, 5),
+    (777, 16, 24, 4, 3, 0),
 ]
 
 
