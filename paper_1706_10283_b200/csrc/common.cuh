@@ -86,7 +86,7 @@ struct ScanArgs {
     int m;
     const uint8_t* qluts;
     int64_t nq;
-    int noshare = 0;      // tcgen05 top-k: no shared thresholds (lists shorter than the final k)
+    int noshare = 0;      // tcgen05 top-k with lists of 32 for k > 32: G = ceil(k/32) threshold groups
 };
 
 }  // namespace bolt

@@ -87,7 +87,6 @@ constexpr int kMmaWarp = kProdWarps + kEpiWarps;
 // SMSP schedulers favour higher warp ids, so the producers, whose one-hot
 // stages gate the MMA, win issue slots over the epilogue's filter work.
 constexpr int kThreads = (kMmaWarp + 1) * 32;
-constexpr int kMaxTopk = 32;
 constexpr int kPrefetch = 3;             // tiles of code words in flight per producer thread
 // u32 words of shared scratch per epilogue thread: top-k parks 32 u16 values
 // (80-byte rows: 16-byte aligned, conflict-free); full output stages a 32-row x
