@@ -102,8 +102,9 @@ constexpr int kFallbackBatch = 48;  // flagged queries per exact fallback batch 
 TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     TopkPlan p{};
     int v = variant;
-    // auto: tensor cores from 24 queries (sweep crossover, profiles/r1/bench_sweep.json), else PRMT
-    if (v == BOLT_VARIANT_AUTO) v = topk_tc_supported(n, m, nq, k) && nq >= 24 ? BOLT_VARIANT_TC : BOLT_VARIANT_PRMT;
+    // auto: tensor cores above 16 queries (sweep crossover with the single-CTA tiles: PRMT runs
+    // query tiles of 8, so 17-24 queries cost three of them), else PRMT
+    if (v == BOLT_VARIANT_AUTO) v = topk_tc_supported(n, m, nq, k) && nq > 16 ? BOLT_VARIANT_TC : BOLT_VARIANT_PRMT;
     p.variant = v;
     p.small = v == BOLT_VARIANT_PRMT && topk_small_supported(n, m, nq, k);
     p.parts = v == BOLT_VARIANT_TC    ? topk_tc_parts(n, m, nq, k, sms)
