@@ -126,11 +126,15 @@ constexpr int kEnc2Threads = 256;
 constexpr int kEnc2Rows = 2;
 constexpr int kEnc2RowsPerBlock = kEnc2Threads * kEnc2Rows;  // 512 = 64 groups
 
+// L = 8 (c2, c4, c5) or 16 (c3): the codebook's L floats of a row are L/8
+// 32-byte loads.
+template <int L>
 __global__ void __launch_bounds__(kEnc2Threads, 2)
 encode_l8_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const float* __restrict__ C, int m,
                  uint32_t* __restrict__ codes) {
     extern __shared__ float4 enc_smem4[];
-    constexpr int L = 8;
+    static_assert(L == 8 || L == 16, "32-byte row slices");
+    constexpr int NL = L / 8;  // 32-byte loads per (row, codebook)
     const int j = m * L;
     float* cneg = reinterpret_cast<float*>(enc_smem4);  // [m][L][16] negated
     uint32_t* stage = reinterpret_cast<uint32_t*>(cneg + (size_t)j * kK);  // [64][m]
@@ -152,23 +156,31 @@ encode_l8_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const floa
         valid[r] = row0 + r < n;
         xr[r] = reinterpret_cast<const float4*>(X + (valid[r] ? (row0 + r) : 0) * ldx);
     }
-    float4 nx[kEnc2Rows][2];
+    float4 nx[kEnc2Rows][2 * NL];
 #pragma unroll
-    for (int r = 0; r < kEnc2Rows; ++r) {
-        if (valid[r]) ldg256(reinterpret_cast<const float*>(xr[r]), nx[r][0], nx[r][1]);
-        else nx[r][0] = nx[r][1] = make_float4(0, 0, 0, 0);
-    }
+    for (int r = 0; r < kEnc2Rows; ++r)
+#pragma unroll
+        for (int h = 0; h < NL; ++h) {
+            if (valid[r]) ldg256(reinterpret_cast<const float*>(xr[r] + 2 * h), nx[r][2 * h], nx[r][2 * h + 1]);
+            else nx[r][2 * h] = nx[r][2 * h + 1] = make_float4(0, 0, 0, 0);
+        }
     for (int c = 0; c < m; ++c) {
         float xv[kEnc2Rows][L];
 #pragma unroll
-        for (int r = 0; r < kEnc2Rows; ++r) {
-            xv[r][0] = nx[r][0].x; xv[r][1] = nx[r][0].y; xv[r][2] = nx[r][0].z; xv[r][3] = nx[r][0].w;
-            xv[r][4] = nx[r][1].x; xv[r][5] = nx[r][1].y; xv[r][6] = nx[r][1].z; xv[r][7] = nx[r][1].w;
-        }
+        for (int r = 0; r < kEnc2Rows; ++r)
+#pragma unroll
+            for (int h = 0; h < 2 * NL; ++h) {
+                xv[r][4 * h] = nx[r][h].x; xv[r][4 * h + 1] = nx[r][h].y;
+                xv[r][4 * h + 2] = nx[r][h].z; xv[r][4 * h + 3] = nx[r][h].w;
+            }
         if (c + 1 < m) {
 #pragma unroll
             for (int r = 0; r < kEnc2Rows; ++r)
-                if (valid[r]) ldg256(reinterpret_cast<const float*>(xr[r] + 2 * (c + 1)), nx[r][0], nx[r][1]);
+                if (valid[r])
+#pragma unroll
+                    for (int h = 0; h < NL; ++h)
+                        ldg256(reinterpret_cast<const float*>(xr[r] + 2 * NL * (c + 1) + 2 * h), nx[r][2 * h],
+                               nx[r][2 * h + 1]);
         }
         float2 d[kEnc2Rows][kK / 2];
 #pragma unroll
@@ -253,10 +265,11 @@ cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const f
     size_t smem = (size_t)j * kK * sizeof(float) + (size_t)kEncGroupsPerBlock * m * sizeof(uint32_t);
     bool vec = (L % 4 == 0) && (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
     int64_t blocks = ceil_div(n, kEncRowsPerBlock);
-    if (vec && L == 8 && (ldx % 8) == 0 && (reinterpret_cast<uintptr_t>(X) & 31) == 0) {
+    if (vec && (L == 8 || L == 16) && (ldx % 8) == 0 && (reinterpret_cast<uintptr_t>(X) & 31) == 0) {
         static_assert(kEnc2RowsPerBlock == kEncRowsPerBlock, "same 64-group staging");
-        cudaFuncSetAttribute(encode_l8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        encode_l8_kernel<<<(unsigned)blocks, kEnc2Threads, smem, s>>>(X, n, ldx, C, m, codes);
+        auto kern = L == 8 ? encode_l8_kernel<8> : encode_l8_kernel<16>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<(unsigned)blocks, kEnc2Threads, smem, s>>>(X, n, ldx, C, m, codes);
     } else if (vec) {
         cudaFuncSetAttribute(encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         encode_kernel<true><<<(unsigned)blocks, kEncThreads, smem, s>>>(X, n, j, ldx, C, m, codes);
