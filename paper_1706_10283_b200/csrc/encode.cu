@@ -129,7 +129,7 @@ constexpr int kEnc2RowsPerBlock = kEnc2Threads * kEnc2Rows;  // 512 = 64 groups
 // L = 8 (c2, c4, c5) or 16 (c3): the codebook's L floats of a row are L/8
 // 32-byte loads.
 template <int L>
-__global__ void __launch_bounds__(kEnc2Threads, 2)
+__global__ void __launch_bounds__(kEnc2Threads, L == 8 ? 3 : 2)
 encode_l8_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const float* __restrict__ C, int m,
                  uint32_t* __restrict__ codes) {
     extern __shared__ float4 enc_smem4[];
