@@ -29,3 +29,5 @@ python bench.py --config c5 --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 0
   ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name regex:"topk|merge|verify|lut" --csv \
   --log-file gpurun_out/launches_bench_c5.csv \
   python bench.py --config c5 --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ncu_c5_launch.log 2>&1
+python bench.py --config c2nq --steps 3 --warmup 3 > gpurun_out/bench_c2nq.json 2> gpurun_out/bench_c2nq.err
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
