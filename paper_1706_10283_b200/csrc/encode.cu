@@ -128,8 +128,10 @@ constexpr int kEnc2RowsPerBlock = kEnc2Threads * kEnc2Rows;  // 512 = 64 groups
 
 // L = 8 (c2, c4, c5) or 16 (c3): the codebook's L floats of a row are L/8
 // 32-byte loads.
-template <int L>
-__global__ void __launch_bounds__(kEnc2Threads, L == 8 ? 3 : 2)
+// THREADS = 256 (512 rows = 64 groups per block) or 128 for small n, where
+// 512-row blocks would leave SMs idle.
+template <int L, int THREADS>
+__global__ void __launch_bounds__(THREADS, L == 8 ? 3 * 256 / THREADS : 2 * 256 / THREADS)
 encode_l8_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const float* __restrict__ C, int m,
                  uint32_t* __restrict__ codes) {
     extern __shared__ float4 enc_smem4[];
@@ -148,7 +150,8 @@ encode_l8_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const floa
     __syncthreads();
     // thread t: rows 4*(t/2) + 2*(t%2) + {0,1}: a pair of threads covers 4 rows,
     // so the 16-bit half-words of a layout-v1 group are built as before
-    const int64_t row0 = (int64_t)blockIdx.x * kEnc2RowsPerBlock + threadIdx.x * kEnc2Rows;
+    constexpr int RPB = THREADS * kEnc2Rows, GPB = RPB / kRowsPerWord;  // rows, groups per block
+    const int64_t row0 = (int64_t)blockIdx.x * RPB + threadIdx.x * kEnc2Rows;
     const float4* xr[kEnc2Rows];
     bool valid[kEnc2Rows];
 #pragma unroll
@@ -225,9 +228,9 @@ encode_l8_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const floa
         if ((threadIdx.x & 3) == 0) stage[(threadIdx.x >> 2) * m + c] = quarter | (q1 << 8) | (q2 << 16) | (q3 << 24);
     }
     __syncthreads();
-    const int64_t g0 = (int64_t)blockIdx.x * kEncGroupsPerBlock;
+    const int64_t g0 = (int64_t)blockIdx.x * GPB;
     const int64_t groups = ceil_div(n, kRowsPerWord);
-    const int64_t ng = min64(kEncGroupsPerBlock, groups - g0);
+    const int64_t ng = min64(GPB, groups - g0);
     uint32_t* dst = codes + g0 * m;
     for (int64_t e = threadIdx.x; e < ng * m; e += blockDim.x) dst[e] = stage[e];
 }
@@ -267,9 +270,20 @@ cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const f
     int64_t blocks = ceil_div(n, kEncRowsPerBlock);
     if (vec && (L == 8 || L == 16) && (ldx % 8) == 0 && (reinterpret_cast<uintptr_t>(X) & 31) == 0) {
         static_assert(kEnc2RowsPerBlock == kEncRowsPerBlock, "same 64-group staging");
-        auto kern = L == 8 ? encode_l8_kernel<8> : encode_l8_kernel<16>;
+        static int sms = 0;
+        if (sms == 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (sms <= 0) sms = 148;
+        }
+        const bool small = blocks < 2 * sms;  // halve the blocks' rows so that every SM gets work
+        auto kern = L == 8 ? (small ? encode_l8_kernel<8, 128> : encode_l8_kernel<8, 256>)
+                           : (small ? encode_l8_kernel<16, 128> : encode_l8_kernel<16, 256>);
+        const int threads = small ? 128 : 256;
+        const int64_t nb = ceil_div(n, (int64_t)threads * kEnc2Rows);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<(unsigned)blocks, kEnc2Threads, smem, s>>>(X, n, ldx, C, m, codes);
+        kern<<<(unsigned)nb, threads, smem, s>>>(X, n, ldx, C, m, codes);
     } else if (vec) {
         cudaFuncSetAttribute(encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         encode_kernel<true><<<(unsigned)blocks, kEncThreads, smem, s>>>(X, n, j, ldx, C, m, codes);
