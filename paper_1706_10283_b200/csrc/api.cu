@@ -394,7 +394,7 @@ bolt_status bolt_scan_dequant(const uint32_t* codes, int64_t n, int m, const uin
 }
 
 size_t bolt_topk_workspace_bytes_ex(int64_t n, int m, int64_t nq, int k, int variant) {
-    if (n < 0 || nq < 0 || k < 1 || k > kMaxK || m < 1 || m > kMaxM) return 0;
+    if (n < 0 || nq <= 0 || k < 1 || k > kMaxK || m < 1 || m > kMaxM) return 0;
     return topk_plan(n, m, nq, k, variant, sms_or_default()).ws;
 }
 

@@ -43,6 +43,7 @@ __device__ __forceinline__ uint64_t make_key(uint32_t kv, uint64_t gidx) {
 // `min_groups_per_task` groups per task, and the partition count in a small
 // window that best fills the last round.
 inline int choose_parts(int64_t tiles, int64_t groups, int64_t W, int64_t min_groups_per_task) {
+    tiles = max64(tiles, 1);  // nq = 0: no work, one partition
     const int64_t max_parts = max64(1, min64(16384, groups / min_groups_per_task));
     int64_t lo = max64(1, ceil_div(4 * W, tiles));
     if (lo >= max_parts) return (int)max_parts;

@@ -651,6 +651,31 @@ def test_code_buffer_grows_and_searches(bolt, orc):
     np.testing.assert_array_equal(keys, orc.topk(orc.unpack_v1(host(cb.codes), 3001, cfg.m), host(ql), 10, 0))
 
 
+# ------------------------------------------------------------ empty inputs
+def test_empty_inputs(bolt):
+    """n = 0 or nq = 0 through every entry point: no launch faults, top-k lists
+    all padding (UINT64_MAX), empty outputs stay empty."""
+    import torch
+    m = 16
+    C = dev(G.random_floats((m, 16, 8), 5))
+    codes0 = bolt.encode(torch.empty((0, 128), dtype=torch.float32, device="cuda"), C)
+    assert codes0.numel() == 0
+    codes = bolt.pack_codes(dev(G.random_codes(100, m, 6)))
+    ql = dev(G.random_qluts(3, m, 7))
+    pad = np.full((3, 10), np.uint64(2**64 - 1))
+    for v in (bolt.VARIANT_AUTO, bolt.VARIANT_PRMT, bolt.VARIANT_TC):
+        np.testing.assert_array_equal(host(bolt.topk(codes, 0, ql, 10, 0, variant=v)), pad)
+    assert host(bolt.topk(codes, 100, ql[:0], 10, 0)).shape == (0, 10)
+    assert host(bolt.scan(codes, 0, ql)).shape == (0, 3)
+    assert host(bolt.scan(codes, 100, ql[:0])).shape == (100, 0)
+    luts = dev(G.random_floats((3, m, 16), 8))
+    np.testing.assert_array_equal(host(bolt.topk_f32(codes, 0, luts, 10, 0)), pad)
+    assert host(bolt.scan_f32(codes, 0, luts)).shape == (0, 3)
+    buf = torch.zeros(bolt.codes_words(8, m), dtype=torch.uint32, device="cuda")
+    bolt.encode_append(torch.empty((0, 128), dtype=torch.float32, device="cuda"), C, buf, 0)
+    assert int(host(buf).sum()) == 0
+
+
 # ------------------------------------------------------- offline fit (f1)
 @pytest.mark.parametrize("cfg_name,n", [("c1", 10_000), ("c2", 20_000), ("c4", 5_000)])
 def test_kmeans_gpu_equals_oracle(bolt, orc, cfg_name, n):
