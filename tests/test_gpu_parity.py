@@ -220,6 +220,13 @@ TOPK_CASES = [
     (20000, 16, 8, 128, 256, 2**40),
     (65537, 16, 3, 10, 8, 0),
     (10000, 64, 4, 64, 256, 0),
+    # small-batch query tiles of 2 and 4 (several tiles), the batched PRMT
+    # kernel (nq >= 64), an index base at the top of the 48-bit range
+    (30001, 16, 6, 10, 16, 0),
+    (30001, 16, 10, 7, 256, 0),
+    (12345, 8, 12, 20, 256, 0),
+    (9000, 16, 70, 10, 8, 0),
+    (4000, 32, 11, 10, 256, 2**48 - 4001),
 ]
 
 
