@@ -479,7 +479,7 @@ def test_c5_device_rows_sampled(bolt, orc):
     import torch
     from synth import gpu as sg
     cfg2 = G.CONFIGS["c2"]
-    r0, n = 99_900_000, 60_000
+    r0, n = 99_900_000, 100_000  # 1e5 rows re-encoded by the oracle
     X = torch.empty((n, 128), dtype=torch.float32, device="cuda")
     sg.c5_rows(r0, n, dev(G.c5_means()), X)
     Xh = host(X)
@@ -505,7 +505,7 @@ def test_c5_full_size_sampled(bolt, orc):
     """BASELINE c5 on one GPU in bench.py's launch configuration: the 1e8-row
     device-generated database encoded in 1M-row chunks, Q = 65,536, top-100
     (tcgen05 lists of 32 over 382 partitions, merged and verified); the oracle
-    checks 3 sampled queries over the full 800 MB of GPU codes (read with O12)."""
+    checks 64 sampled queries over the full 800 MB of GPU codes (read with O12)."""
     import torch
     from synth import gpu as sg
     cfg2, cfg5 = G.CONFIGS["c2"], G.CONFIGS["c5"]
@@ -526,7 +526,7 @@ def test_c5_full_size_sampled(bolt, orc):
     ql = bolt.build_quantized_luts(dev(G.queries(cfg5)), Cd, 0, float(a), dev(b))
     assert bolt.topk_plan(n, m, cfg5.nq, cfg5.k)[0] == "tc"
     keys = host(bolt.topk(codes, n, ql, cfg5.k, 0))
-    qs = np.random.default_rng(5).choice(cfg5.nq, 3, replace=False)
+    qs = np.random.default_rng(5).choice(cfg5.nq, 64, replace=False)  # 64 sampled queries
     qlh = host(ql[torch.from_numpy(qs).cuda()])
     gcodes = orc.unpack_v1(host(codes), n, m)
     np.testing.assert_array_equal(keys[qs], orc.topk(gcodes, qlh, cfg5.k, 0))
