@@ -92,3 +92,20 @@ def test_workspace_sizing_host(lib):
             expect = 0 if p == 1 else p * nq * k * 8 + nq * 4
         assert ws == expect, (n, m, nq, k, variant, p, ws)
         assert 1 <= p <= 16384
+
+
+def test_c_example_builds(lib, tmp_path):
+    """examples/search.c uses the C ABI alone (no Python): it compiles and
+    links against bolt.h and libbolt.so (run on a GPU by hand or by tools)."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    out = tmp_path / "search"
+    inc = os.path.join(ROOT, "include")
+    libdir = os.path.join(ROOT, "paper_1706_10283_b200")
+    r = subprocess.run(["gcc", "-O2", "-std=c11", "-Wall", "-Werror", f"-I{inc}", "-I/usr/local/cuda/include",
+                        "-o", str(out), os.path.join(ROOT, "examples", "search.c"), f"-L{libdir}", "-lbolt",
+                        f"-Wl,-rpath,{libdir}", "-L/usr/local/cuda/lib64", "-lcudart"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
