@@ -174,7 +174,10 @@ BOLT_API bolt_status bolt_scan_dequant_ex(const uint32_t* codes, int64_t n, int 
  *   out_keys [nq][k] u64, sorted ascending; UINT64_MAX padding when k > n.
  *   1 <= k <= 128; index_base + n <= 2^48.
  *   ws: device scratch of at least bolt_topk_workspace_bytes(n, m, nq, k)
- *   bytes (8 B aligned). */
+ *   bytes (8 B aligned).
+ * Asynchronous on `stream`, except on the tcgen05 path with k > 32: lists of
+ * 32 are merged and checked, and the call waits for one count of queries
+ * that need the exact PRMT rescan (not CUDA-graph capturable). */
 BOLT_API size_t bolt_topk_workspace_bytes(int64_t n, int m, int64_t nq, int k);
 BOLT_API bolt_status bolt_topk(const uint32_t* codes, int64_t n, int m, const uint8_t* qluts, int64_t nq,
                       int k, bolt_metric metric, int64_t index_base, uint64_t* out_keys, void* ws,
