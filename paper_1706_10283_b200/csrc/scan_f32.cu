@@ -12,6 +12,8 @@
 //
 // Keys (R18): the float's order-preserving code (negative: bits flipped, else
 // the sign bit set; inverted for the dot product) << 32 | global index.
+#include <cmath>
+
 #include "common.cuh"
 
 namespace bolt {
@@ -101,17 +103,36 @@ topk_f32_kernel(const uint32_t* __restrict__ codes, int64_t n, int m, const floa
     const int64_t r0 = part * rows_per_warp;
     const int64_t r1 = min64(n, r0 + rows_per_warp);
     const int nv = (int)min64(kF32QT, nq - q0);
+    // per-query threshold in registers (the same in every lane): the value of
+    // the list's k-th key once the list is full; a lane's value is a
+    // candidate if it is at least as good (ties are settled on the full key)
+    const bool dot = metric == BOLT_DOT;
+    float thr[kF32QT];
+#pragma unroll
+    for (int q = 0; q < kF32QT; ++q) thr[q] = dot ? -INFINITY : INFINITY;
     for (int64_t base = r0; base < r1; base += 32) {
         const int64_t row = base + lane;
         const bool valid = row < r1;
         float acc[kF32QT];
         row_sums(codes, valid ? row : r0, m, f32_tab, acc);
+        uint32_t mask = 0;
 #pragma unroll
         for (int q = 0; q < kF32QT; ++q) {
-            if (q >= nv) break;
+            const bool c = q < nv && valid && (dot ? acc[q] >= thr[q] : acc[q] <= thr[q]);
+            mask |= (uint32_t)c << q;
+        }
+        uint32_t any = __reduce_or_sync(0xffffffffu, mask);
+        while (any) {
+            const int q = __ffs(any) - 1;
+            any &= any - 1;
             uint64_t* list = lists + q * k;
-            const uint64_t key = valid ? key_f32(acc[q], (uint64_t)(index_base + row), metric) : ~0ull;
+            // this query's value of the lane (dynamic q: select from registers)
+            float v = 0.f;
+#pragma unroll
+            for (int t = 0; t < kF32QT; ++t) v = t == q ? acc[t] : v;
+            const uint64_t key = (mask >> q) & 1u ? key_f32(v, (uint64_t)(index_base + row), metric) : ~0ull;
             uint32_t cand = __ballot_sync(0xffffffffu, key < list[k - 1]);
+            uint64_t kth = ~0ull;
             while (cand) {
                 const int src = __ffs(cand) - 1;
                 cand &= cand - 1;
@@ -127,6 +148,15 @@ topk_f32_kernel(const uint32_t* __restrict__ codes, int64_t n, int m, const floa
                 __syncwarp();
                 if (lane < k) list[lane] = nw;
                 __syncwarp();
+            }
+            kth = list[k - 1];
+            if (kth != ~0ull) {  // full: the k-th value bounds the list
+                uint32_t ord = (uint32_t)(kth >> 32);
+                if (dot) ord = ~ord;
+                const float kv = __uint_as_float((ord & 0x80000000u) ? (ord & 0x7FFFFFFFu) : ~ord);
+#pragma unroll
+                for (int t = 0; t < kF32QT; ++t)
+                    if (t == q) thr[t] = kv;
             }
         }
     }
