@@ -102,9 +102,11 @@ constexpr int kFallbackBatch = 48;  // flagged queries per exact fallback batch 
 TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     TopkPlan p{};
     int v = variant;
-    // auto: tensor cores above 16 queries (sweep crossover with the single-CTA tiles: PRMT runs
-    // query tiles of 8, so 17-24 queries cost three of them), else PRMT
-    if (v == BOLT_VARIANT_AUTO) v = topk_tc_supported(n, m, nq, k) && nq > 16 ? BOLT_VARIANT_TC : BOLT_VARIANT_PRMT;
+    // auto: tensor cores above a per-M query count, else PRMT.  Crossovers measured on 10^8
+    // rows: M = 16 TC 3.0 ms flat for Q <= 128 vs PRMT 2.57 (Q = 12) / 3.24
+    // (Q = 13); M = 8 even at Q = 20; M = 32 (pair tiles) even at Q = 16.
+    const int64_t tc_above = m == 16 ? 12 : (m == 8 ? 20 : 16);
+    if (v == BOLT_VARIANT_AUTO) v = topk_tc_supported(n, m, nq, k) && nq > tc_above ? BOLT_VARIANT_TC : BOLT_VARIANT_PRMT;
     p.variant = v;
     p.small = v == BOLT_VARIANT_PRMT && topk_small_supported(n, m, nq, k);
     p.parts = v == BOLT_VARIANT_TC    ? topk_tc_parts(n, m, nq, k, sms)
