@@ -18,12 +18,18 @@ scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "m
 start_k = sys.argv[3] if len(sys.argv) > 3 else "encode"
 end_k = sys.argv[4] if len(sys.argv) > 4 else "merge_kernel"
 enc = [i for i, (k, _, _) in enumerate(launches) if start_k in k]
+# complete steps only: a start kernel followed by an end kernel before the next start
+# (bench.py's e2e/roofline legs launch partial sequences after the timed steps)
+bounds = enc[1:] + [len(launches)]
+complete = []
+for e, nxt in zip(enc, bounds):
+    ends = [j for j in range(e, nxt) if end_k in launches[j][0]]
+    if ends:
+        complete.append((e, ends[0]))
 tot = collections.defaultdict(float)
-for e in enc[-steps:]:  # one step = encode .. the first merge after it
-    for k, v, u in launches[e:]:
+for e, last in complete[-steps:]:  # one step = start kernel .. the first end kernel after it
+    for k, v, u in launches[e:last + 1]:
         tot[k.split("(")[0]] += v * scale.get(u, 1e-6)
-        if end_k in k:
-            break
 step = sum(tot.values()) / steps
 print(json.dumps({"source": sys.argv[1], "steps": steps, "step_ms": round(step, 4),
                   "share": {k: round(v / steps / step, 4) for k, v in tot.items()}}, indent=1))
