@@ -184,7 +184,10 @@ BOLT_API bolt_status bolt_topk(const uint32_t* codes, int64_t n, int m, const ui
                       size_t ws_bytes, bolt_stream_t stream);
 /* The plan bolt_topk_ex will use for these shapes (host): the resolved
  * variant (BOLT_VARIANT_PRMT / BOLT_VARIANT_TC) and the number of row
- * partitions whose partial lists are merged (1 = no merge). */
+ * partitions whose partial lists are merged (1 = no merge).  AUTO picks
+ * tcgen05 for m in {8, 16, 32}, k <= 128 and nq above 20 (m = 8), 12
+ * (m = 16) or 16 (m = 32) — crossovers measured on 10^8 rows (DESIGN.md
+ * §1) — else PRMT; the results are the same keys either way. */
 BOLT_API bolt_status bolt_topk_plan(int64_t n, int m, int64_t nq, int k, int variant,
                                     int* resolved_variant, int* parts);
 /* As bolt_topk with an explicit scan variant (tests, benchmarks). */
