@@ -172,7 +172,7 @@ BOLT_API bolt_status bolt_scan_dequant_ex(const uint32_t* codes, int64_t n, int 
  *   DOT : key = ((0xFFFF - acc) << 48) | (index_base + i)
  * ascending, so best first and ties broken by the lower global index.
  *   out_keys [nq][k] u64, sorted ascending; UINT64_MAX padding when k > n.
- *   1 <= k <= 128; index_base + n <= 2^48.
+ *   1 <= k <= 128; index_base + n < 2^48 (index 2^48 - 1 with value 0xFFFF would equal the padding key).
  *   ws: device scratch of at least bolt_topk_workspace_bytes(n, m, nq, k)
  *   bytes (8 B aligned).
  * Asynchronous on `stream`, except on the tcgen05 path with k > 32: lists of
