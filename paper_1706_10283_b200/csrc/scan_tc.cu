@@ -1203,7 +1203,7 @@ int topk_tc_parts(int64_t n, int m, int64_t nq, int k, int num_sms) {
     const bool single = tc::tc_single(nq, m, k, k > 32 ? 1 : 0);  // k > 32: pair lists of 32 (api.cu)
     const int64_t tiles_q = ceil_div(nq, (single ? 1 : 2) * tc::kQM);
     const int64_t max_range = m == 8 ? tc::Cfg<8>::MAX_RANGE : (m == 16 ? tc::Cfg<16>::MAX_RANGE : tc::Cfg<32>::MAX_RANGE);
-    // finer units where one query tile spans the batch (measured: DESIGN.md §4 "Unit count")
+    // finer units where one query tile spans the batch (measured: DESIGN.md §6.1 "Unit count")
     const int64_t W = single ? 4 * num_sms : (m == 32 && tiles_q == 1 ? num_sms : num_sms / 2);
     int rparts = choose_parts(tiles_q, ceil_div(n, 8), W, (int64_t)256 * 16 / 8);
     rparts = (int)max64(rparts, ceil_div(n, max_range - 8));
