@@ -177,9 +177,11 @@ static const double ALPHA_GRID[8] = {0.0, 0.001, 0.002, 0.005, 0.01, 0.02, 0.05,
  * tables (R2, R3), then the mean squared reconstruction error of
  * yhat = beta/a + b_m (R1).  The first alpha with the strictly
  * smallest error wins (R4).  Outputs are fp64; the model stores them as fp32.
- * mse_out (optional) receives the 8 grid errors. */
-void oracle_calibrate(const double* D, int64_t nq, int M, double* a_out, double* b_out,
-                      double* alpha_out, double* mse_out) {
+ * mse_out (optional) receives the 8 grid errors; a_grid [8] and b_grid [8][M]
+ * (optional) the (a, b_m) of every grid alpha, so that each quantile can be
+ * checked on its own, not only the winner's. */
+void oracle_calibrate_grid(const double* D, int64_t nq, int M, double* a_out, double* b_out,
+                           double* alpha_out, double* mse_out, double* a_grid, double* b_grid) {
     const int64_t per_table = nq * K;
     const int64_t total = per_table * M;
     double* col = (double*)malloc(sizeof(double) * per_table);
@@ -219,6 +221,8 @@ void oracle_calibrate(const double* D, int64_t nq, int M, double* a_out, double*
                 }
         double mse = sse / (double)total;
         if (mse_out) mse_out[g] = mse;
+        if (a_grid) a_grid[g] = a;
+        if (b_grid) memcpy(b_grid + (int64_t)g * M, b, sizeof(double) * M);
         if (mse < best_mse) {
             best_mse = mse;
             best_a = a;
@@ -234,6 +238,11 @@ void oracle_calibrate(const double* D, int64_t nq, int M, double* a_out, double*
     free(pooled);
     free(b);
     free(best_b);
+}
+
+void oracle_calibrate(const double* D, int64_t nq, int M, double* a_out, double* b_out,
+                      double* alpha_out, double* mse_out) {
+    oracle_calibrate_grid(D, nq, M, a_out, b_out, alpha_out, mse_out, NULL, NULL);
 }
 
 /* ---------------------------------------------------------------- O2 -- */

@@ -46,6 +46,7 @@ def lib():
             "oracle_luts": ([P, i64, i32, P, i32, i32, P], None),
             "oracle_quantize": ([P, i64, i32, f32, P, P, P], None),
             "oracle_calibrate": ([P, i64, i32, P, P, P, P], None),
+            "oracle_calibrate_grid": ([P, i64, i32, P, P, P, P, P, P], None),
             "oracle_kmeans_subspace": ([P, i64, i32, i32, i32, P, i32, P, P], None),
             "oracle_scan": ([P, i64, i32, P, i64, P], None),
             "oracle_topk": ([P, i64, i32, P, i64, i32, i32, i64, P], None),
@@ -123,6 +124,21 @@ def calibrate(D):
     mse = np.zeros(8, np.float64)
     lib().oracle_calibrate(_p(D), nq, M, _p(a), _p(b), _p(alpha), _p(mse))
     return float(a[0]), b, float(alpha[0]), mse
+
+
+def calibrate_grid(D):
+    """O5 with every grid point exposed: -> (a [8], b [8][M], mse [8]) in fp64,
+    row g for alpha = ALPHA_GRID[g]."""
+    D = np.ascontiguousarray(D, dtype=np.float64)
+    nq, M, _ = D.shape
+    a, alpha = np.zeros(1), np.zeros(1)
+    b = np.zeros(M)
+    mse, ag, bg = np.zeros(8), np.zeros(8), np.zeros((8, M))
+    lib().oracle_calibrate_grid(_p(D), nq, M, _p(a), _p(b), _p(alpha), _p(mse), _p(ag), _p(bg))
+    return ag, bg, mse
+
+
+ALPHA_GRID = (0.0, 0.001, 0.002, 0.005, 0.01, 0.02, 0.05, 0.1)  # P:L289
 
 
 def kmeans(train, M: int, init, iters: int = 16, with_inertia: bool = False):

@@ -196,6 +196,53 @@ def test_calibrate_nearest_rank_matches_numpy(orc):
     assert mse[grid.index(alpha)] == pytest.approx(((yhat - D) ** 2).mean(), rel=1e-12)
 
 
+def _nearest_rank_checks(orc, D):
+    """Every grid alpha (not only the winner): b_m = F_m^-1(alpha) and
+    a = 255 / F^-1(1 - alpha) of the pooled residuals, both numpy's
+    'inverted_cdf' quantile (library routine), and the grid error recomputed
+    from P:L283-286."""
+    ag, bg, mse = orc.calibrate_grid(D)
+    M = D.shape[1]
+    for g, alpha in enumerate(orc.ALPHA_GRID):
+        for m in range(M):
+            assert bg[g, m] == np.quantile(D[:, m, :].ravel(), alpha, method="inverted_cdf"), (alpha, m)
+        resid = (D - bg[g][None, :, None]).ravel()
+        assert ag[g] == 255.0 / np.quantile(resid, 1 - alpha, method="inverted_cdf"), alpha
+        beta = np.clip(np.floor(ag[g] * (D - bg[g][None, :, None])), 0, 255)
+        yhat = beta / ag[g] + bg[g][None, :, None]
+        assert mse[g] == pytest.approx(((yhat - D) ** 2).mean(), rel=1e-12)
+    return ag, bg, mse
+
+
+def test_calibrate_every_alpha_tail_heavy(orc):
+    """P:L289 at alpha > 0: a bulk on [0, 1) with one far outlier above it and
+    one below, 200,000 entries per table, so alpha n is an integer at every
+    grid point (0.001 n = 200): the nearest rank max(ceil(p n) - 1, 0) and
+    floor(p n) pick different entries there, and only the former is numpy's
+    inverted CDF.  Clipping the two outliers costs (256^2 + 200^2) / 400,000
+    in MSE, less than alpha = 0's resolution loss (step ~1), so the winner is
+    alpha = 0.001 (R4), and the returned (a, b) are that grid point's."""
+    rng = np.random.default_rng(7)
+    D = rng.uniform(0.0, 1.0, (12_500, 2, 16))
+    D[17, 0, 3], D[5, 1, 1] = 256.0, -200.0
+    ag, bg, mse = _nearest_rank_checks(orc, D)
+    a, b, alpha, mse2 = orc.calibrate(D)
+    assert alpha == 0.001 and int(np.argmin(mse)) == 1
+    assert a == ag[1] and (b == bg[1]).all()
+    np.testing.assert_array_equal(mse, mse2)
+    # the two picks differ by one rank here (a continuous sample has no ties)
+    s0 = np.sort(D[:, 0, :].ravel())
+    assert bg[1, 0] == s0[199] != s0[200]
+
+
+def test_calibrate_every_alpha_gamma(orc):
+    """Same per-alpha checks on the gamma tables where alpha = 0 wins, with
+    n = 40 x 16 = 640 per table (alpha n not an integer: ceil - 1 = floor)."""
+    rng = np.random.default_rng(7)
+    D = rng.gamma(2.0, 3.0, (40, 4, 16)) + np.arange(4)[None, :, None] * 10
+    _nearest_rank_checks(orc, D)
+
+
 def test_calibrate_constant_and_uniform(orc):
     """Constant tables: b = c, beta = 0, MSE 0.  Uniform entries:
     floor quantization error is U[0, 1/a), so MSE = (1/a)^2 / 3 (R5/R17)."""
@@ -329,6 +376,23 @@ def test_kmeans_empty_cluster_takes_farthest(orc):
     assert C[0, 1, 0] == 50.0
     assert C[0, 0, 0] == pytest.approx((0.0 + float(np.float32(0.1)) + float(np.float32(0.2)) + 50.0) / 4, rel=1e-15)
     np.testing.assert_array_equal(C[0, 2:, 0], pts[4:, 0])
+
+
+def test_kmeans_two_empty_clusters_take_distinct_rows(orc):
+    """R8 with two clusters empty in one iteration: centroids 0, 1, 2 all
+    start at row 0, so assignment ties give every nearby point to centroid 0
+    and leave 1 and 2 empty.  In ascending k, centroid 1 takes the farthest
+    point (row 3, 50: equidistant from 0 and 100, so assigned to centroid 0,
+    distance 2500) and centroid 2 the farthest row NOT already taken this
+    iteration (row 4, 30: distance 900) -- never row 3 twice."""
+    vals = [0.0, 0.1, 0.2, 50.0, 30.0] + [100.0 + i for i in range(13)]
+    pts = np.array(vals, np.float32)[:, None]
+    init = np.array([[0, 0, 0] + list(range(5, 18))])
+    C = orc.kmeans(pts, 1, init, iters=1)
+    assert C[0, 1, 0] == 50.0 and C[0, 2, 0] == 30.0
+    f = [float(np.float32(v)) for v in vals[:5]]
+    assert C[0, 0, 0] == ((((f[0] + f[1]) + f[2]) + f[3]) + f[4]) / 5  # row-order sum (R8)
+    np.testing.assert_array_equal(C[0, 3:, 0], pts[5:, 0])
 
 
 # ------------------------------------------------------------ Lemmas 3 / 4
