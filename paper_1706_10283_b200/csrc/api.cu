@@ -124,10 +124,16 @@ TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     if (v == BOLT_VARIANT_TC && k > kTcListMax) {
         // flags [nq] u32, count, then the exact fallback for flagged queries in
         // batches of kFallbackBatch: gathered tables, keys, small-batch workspace
+        // -- sized for every batch size 1..kFallbackBatch (the last batch is
+        // smaller, and fewer queries may take more row partitions)
+        size_t fb_ws = 0;
+        for (int nb = 1; nb <= kFallbackBatch; ++nb) {
+            const size_t w = topk_plan(n, m, nb, k, BOLT_VARIANT_PRMT, sms).ws;
+            fb_ws = w > fb_ws ? w : fb_ws;
+        }
         p.large_off = align256(p.ws);
         p.ws = p.large_off + align256((size_t)nq * sizeof(uint32_t) + 16) + align256((size_t)kFallbackBatch * m * kK) +
-               align256((size_t)kFallbackBatch * k * sizeof(uint64_t)) +
-               align256(topk_plan(n, m, kFallbackBatch, k, BOLT_VARIANT_PRMT, sms).ws);
+               align256((size_t)kFallbackBatch * k * sizeof(uint64_t)) + align256(fb_ws);
     }
     return p;
 }
@@ -161,7 +167,7 @@ bolt_status bolt_encode(const float* X, int64_t n, int j, int64_t ldx, const flo
     if (!aligned(C, 16)) return fail(BOLT_E_ALIGN, "bolt_encode: C must be 16-byte aligned");
     DevInfo d;
     TRY(device_info(&d));
-    return cuda_status(launch_encode(X, n, j, ldx, C, m, codes, (cudaStream_t)stream), "bolt_encode");
+    return cuda_status(launch_encode(X, n, j, ldx, C, m, codes, d.sms, (cudaStream_t)stream), "bolt_encode");
 }
 
 // ---- Bolt No Quantize (scan_f32.cu)
@@ -242,7 +248,7 @@ bolt_status bolt_encode_append(const float* X, int64_t n_new, int j, int64_t ldx
     if (!aligned(C, 16)) return fail(BOLT_E_ALIGN, "bolt_encode_append: C must be 16-byte aligned");
     DevInfo d;
     TRY(device_info(&d));
-    return cuda_status(launch_encode_append(X, n_new, j, ldx, C, m, codes, n_old, (cudaStream_t)stream),
+    return cuda_status(launch_encode_append(X, n_new, j, ldx, C, m, codes, n_old, d.sms, (cudaStream_t)stream),
                        "bolt_encode_append");
 }
 

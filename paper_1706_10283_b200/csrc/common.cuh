@@ -96,8 +96,9 @@ struct ScanArgs {
 // Implemented in the .cu files, called by api.cu after validation.  They
 // return cudaGetLastError() of their launch.
 namespace bolt {
+// sms: the device's SM count (block-size heuristic), passed down from the ABI's device cache
 cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,
-                          uint32_t* codes, cudaStream_t s);
+                          uint32_t* codes, int sms, cudaStream_t s);
 // Bolt No Quantize (scan_f32.cu): fp32 tables, fp32 sums, R18 keys
 int topk_f32_parts(int64_t n, int64_t nq, int num_sms);
 cudaError_t launch_scan_f32(const uint32_t* codes, int64_t n, int m, const float* luts, int64_t nq, float* out,
@@ -107,7 +108,7 @@ cudaError_t launch_topk_f32(const uint32_t* codes, int64_t n, int m, const float
 cudaError_t launch_keys_split_f32(const uint64_t* keys, int64_t count, int metric, float* vals, int64_t* idx,
                                   cudaStream_t s);
 cudaError_t launch_encode_append(const float* X, int64_t n_new, int j, int64_t ldx, const float* C, int m,
-                                 uint32_t* codes, int64_t n_old, cudaStream_t s);
+                                 uint32_t* codes, int64_t n_old, int sms, cudaStream_t s);
 cudaError_t launch_pack(const uint8_t* flat, int64_t n, int m, uint32_t* codes, cudaStream_t s);
 cudaError_t launch_unpack(const uint32_t* codes, int64_t n, int m, uint8_t* flat, cudaStream_t s);
 

@@ -262,7 +262,7 @@ __global__ void unpack_kernel(const uint32_t* __restrict__ codes, int64_t n, int
 }  // namespace
 
 cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,
-                          uint32_t* codes, cudaStream_t s) {
+                          uint32_t* codes, int sms, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const int L = j / m;
     size_t smem = (size_t)j * kK * sizeof(float) + (size_t)kEncGroupsPerBlock * m * sizeof(uint32_t);
@@ -270,13 +270,6 @@ cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const f
     int64_t blocks = ceil_div(n, kEncRowsPerBlock);
     if (vec && (L == 8 || L == 16) && (ldx % 8) == 0 && (reinterpret_cast<uintptr_t>(X) & 31) == 0) {
         static_assert(kEnc2RowsPerBlock == kEncRowsPerBlock, "same 64-group staging");
-        static int sms = 0;
-        if (sms == 0) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            if (sms <= 0) sms = 148;
-        }
         const bool small = blocks < 2 * sms;  // halve the blocks' rows so that every SM gets work
         auto kern = L == 8 ? (small ? encode_l8_kernel<8, 128> : encode_l8_kernel<8, 256>)
                            : (small ? encode_l8_kernel<16, 128> : encode_l8_kernel<16, 256>);
@@ -324,7 +317,7 @@ __global__ void append_head_kernel(const float* __restrict__ X, int h, int j, in
 }
 
 cudaError_t launch_encode_append(const float* X, int64_t n_new, int j, int64_t ldx, const float* C, int m,
-                                 uint32_t* codes, int64_t n_old, cudaStream_t s) {
+                                 uint32_t* codes, int64_t n_old, int sms, cudaStream_t s) {
     if (n_new == 0) return cudaSuccess;
     const int pos = (int)(n_old % kRowsPerWord);
     const int64_t h = pos == 0 ? 0 : min64(kRowsPerWord - pos, n_new);
@@ -335,7 +328,7 @@ cudaError_t launch_encode_append(const float* X, int64_t n_new, int j, int64_t l
         if (e != cudaSuccess) return e;
     }
     if (n_new == h) return cudaSuccess;
-    return launch_encode(X + h * ldx, n_new - h, j, ldx, C, m, codes + ((n_old + h) / kRowsPerWord) * m, s);
+    return launch_encode(X + h * ldx, n_new - h, j, ldx, C, m, codes + ((n_old + h) / kRowsPerWord) * m, sms, s);
 }
 
 cudaError_t launch_pack(const uint8_t* flat, int64_t n, int m, uint32_t* codes, cudaStream_t s) {

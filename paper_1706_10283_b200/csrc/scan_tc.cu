@@ -916,6 +916,13 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
                         sv[i] = make_uint4(p[c][4 * i], p[c][4 * i + 1], p[c][4 * i + 2], p[c][4 * i + 3]);
+                    // The mask's bit order is not column order (bit 8i + r <->
+                    // column 4r + i), so a candidate may follow a higher-index
+                    // one of the same chunk.  Its own-list test is therefore on
+                    // the full 32-bit key (value, then index), never the value
+                    // alone: a lower index with the k-th key's value still
+                    // displaces it.  The shared bounds (kv <= T) already hold
+                    // for every mask bit.
                     while (mask) {
                         BOLT_PROF_WARP(16, 0);  // warp iterations of the candidate loop
                         const int bpos = __ffs(mask) - 1;
@@ -923,8 +930,9 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                         const int j = 4 * (bpos & 7) + (bpos >> 3);
                         const uint32_t v = (scratch[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
                         const uint32_t kv = kDot ? C::KVMAX - v : v;
-                        if (kv < thr && j < nleft) {
-                            list.insert((kv << C::IDX_BITS) | (uint32_t)(tbl + col + j));
+                        const uint32_t key = (kv << C::IDX_BITS) | (uint32_t)(tbl + col + j);
+                        if (key < list.v[KMAX - 1] && j < nleft) {
+                            list.insert(key);
                             own = list.threshold(C::IDX_BITS);
                             thr = min(thr, own);
                             changed = true;

@@ -395,12 +395,49 @@ def test_host_search_pipelined(bolt, orc, c1_model, chunks):
     np.testing.assert_array_equal(k1.numpy(), orc.topk(orc.unpack_v1(host(codes), cfg.n, cfg.m), host(ql), 10, 0))
 
 
-# ----------------------------------------------------- c2 at full size (sampled)
+# ------------------------------------------- c2 / c3 at full size (all queries)
+def _e2e_trace(orc, X, Q, C, a, b, metric, gcodes, qlg, keys_g, k):
+    """End-to-end parity from raw X and Q (SURVEY 8(c) last contract row):
+    the oracle's own pipeline -- O3 encode, O4 tables, O6 quantize, O8 top-k
+    -- against the GPU's keys.  Every difference must trace to an exempted
+    near-tie upstream: a query whose tables differ (|t - rint t| < 1e-3), or a
+    row whose code differs (relative centroid gap < 1e-5) inside one of the
+    two lists.  Returns (key overlap, queries differing, table near-ties,
+    code near-ties)."""
+    ocodes, gap = orc.encode(X, C, with_gap=True)
+    dcode = gcodes != ocodes
+    assert (dcode <= (gap < 1e-5)).all(), "code mismatch that is not a near-tie"
+    assert dcode.sum() <= NEAR_TIE_CAP * dcode.size
+    D = orc.luts(Q, C, metric)
+    qlo, t = orc.quantize(D, a, b, with_t=True)
+    dtab = qlg != qlo
+    assert (dtab <= (np.abs(t - np.rint(t)) < 1e-3)).all(), "table mismatch that is not a near-tie"
+    assert dtab.sum() <= NEAR_TIE_CAP * dtab.size
+    keys_o = orc.topk(ocodes, qlo, k, metric)            # the oracle alone, from X and Q
+    keys_mid = orc.topk(ocodes, qlg, k, metric)          # oracle codes, GPU tables
+    qtab = dtab.reshape(len(Q), -1).any(axis=1)
+    a_diff = (keys_o != keys_mid).any(axis=1)
+    assert (a_diff <= qtab).all(), "a top-k difference with identical tables and codes"
+    rows_bad = set(np.flatnonzero(dcode.any(axis=1)).tolist())
+    _, i_mid = orc.keys_split(keys_mid, metric)
+    _, i_g = orc.keys_split(keys_g, metric)
+    for q in np.flatnonzero((keys_mid != keys_g).any(axis=1)):
+        involved = set(i_mid[q].tolist()) | set(i_g[q].tolist())
+        assert involved & rows_bad, f"query {q}: differs with no near-tie code in either list"
+    _, i_o = orc.keys_split(keys_o, metric)
+    overlap = np.mean([len(set(i_o[q]) & set(i_g[q])) / k for q in range(len(Q))])
+    ndiff = int((keys_o != keys_g).any(axis=1).sum())
+    print(f"e2e: key overlap {overlap:.6f}, {ndiff} of {len(Q)} queries differ; near-ties: "
+          f"{int(dtab.sum())} table entries, {int(dcode.sum())} codes")
+    return overlap, ndiff, int(dtab.sum()), int(dcode.sum())
+
+
 @pytest.mark.slow
-def test_c2_full_size_sampled(bolt, orc):
+def test_c2_full_size_all_queries(bolt, orc):
     """BASELINE c2 (N=1M, J=128, M=16, Q=10k, top-10) in the launch configuration
-    bench.py times; the oracle checks 16 sampled queries over the full GPU code
-    set (read with O12) and 20k sampled rows of the encoder."""
+    bench.py times: ALL 10,000 queries' keys bit-exact against the oracle's
+    scan of the full GPU code set (read with O12), plus the end-to-end trace
+    from raw X and Q."""
     cfg = G.CONFIGS["c2"]
     X = G.database(cfg)
     train = G.training(cfg, 20_000)
@@ -411,38 +448,33 @@ def test_c2_full_size_sampled(bolt, orc):
     Xd, Qd = dev(X), dev(Q)
     codes = bolt.encode(Xd, dev(C))
     ql = bolt.build_quantized_luts(Qd, dev(C), 0, float(a), dev(b))
+    assert bolt.topk_plan(cfg.n, cfg.m, cfg.nq, cfg.k)[0] == "tc"
     keys = host(bolt.topk(codes, cfg.n, ql, cfg.k, 0))
     gcodes = orc.unpack_v1(host(codes), cfg.n, cfg.m)
-    rows = np.random.default_rng(1).choice(cfg.n, 20_000, replace=False)
-    ref_codes, gap = orc.encode(X[rows], C, with_gap=True)
-    d = gcodes[rows] != ref_codes
-    assert (d <= (gap < 1e-5)).all() and d.sum() <= NEAR_TIE_CAP * d.size
-    qs = np.random.default_rng(2).choice(cfg.nq, 16, replace=False)
     qlh = host(ql)
-    np.testing.assert_array_equal(keys[qs], orc.topk(gcodes, qlh[qs], cfg.k, 0))
+    np.testing.assert_array_equal(keys, orc.topk(gcodes, qlh, cfg.k, 0))
+    _e2e_trace(orc, X, Q, C, a, b, 0, gcodes, qlh, keys, cfg.k)
 
 
 @pytest.mark.slow
-def test_c3_full_size_sampled(bolt, orc):
+def test_c3_full_size_all_queries(bolt, orc):
     """BASELINE c3 (N=1M, J=512, M=32, Q=1k, dot product, top-10 MIPS) in the
-    bench launch configuration: 16 sampled queries checked by the oracle over
-    the full GPU code set; 10k sampled rows re-encoded by the oracle."""
+    bench launch configuration: all 1,000 queries bit-exact against the
+    oracle over the full GPU code set, plus the end-to-end trace."""
     cfg = G.CONFIGS["c3"]
     X = G.database(cfg)
     train = G.training(cfg, 10_000)
     C = orc.fit(train, cfg.m, G.kmeans_init_all(cfg, len(train)), 3)
     a, b, _ = orc.fit_quantizer(G.calibration(cfg, train)[:200], C, 1)
+    Q = G.queries(cfg)
     codes = bolt.encode(dev(X), dev(C))
-    ql = bolt.build_quantized_luts(dev(G.queries(cfg)), dev(C), 1, float(a), dev(b))
+    ql = bolt.build_quantized_luts(dev(Q), dev(C), 1, float(a), dev(b))
     assert bolt.topk_plan(cfg.n, cfg.m, cfg.nq, cfg.k)[0] == "tc"
     keys = host(bolt.topk(codes, cfg.n, ql, cfg.k, 1))
     gcodes = orc.unpack_v1(host(codes), cfg.n, cfg.m)
-    rows = np.random.default_rng(3).choice(cfg.n, 10_000, replace=False)
-    ref_codes, gap = orc.encode(X[rows], C, with_gap=True)
-    d = gcodes[rows] != ref_codes
-    assert (d <= (gap < 1e-5)).all() and d.sum() <= NEAR_TIE_CAP * d.size
-    qs = np.random.default_rng(4).choice(cfg.nq, 16, replace=False)
-    np.testing.assert_array_equal(keys[qs], orc.topk(gcodes, host(ql)[qs], cfg.k, 1))
+    qlh = host(ql)
+    np.testing.assert_array_equal(keys, orc.topk(gcodes, qlh, cfg.k, 1))
+    _e2e_trace(orc, X, Q, C, a, b, 1, gcodes, qlh, keys, cfg.k)
 
 
 @pytest.mark.slow
@@ -582,6 +614,24 @@ def test_scan_f32_bit_exact(bolt, orc, n, m, nq):
     np.testing.assert_array_equal(got, orc.scan_f32(flat, luts))
 
 
+@pytest.mark.parametrize("n,m,nq", [(5000, 16, 40), (3001, 64, 7), (999, 5, 33)])
+def test_scan_f32_within_fp64_bound(bolt, n, m, nq):
+    """The GPU's No-Quantize sums against the exact (fp64) sum of the same fp32
+    entries -- not against O13's fp32 order: the recursive-summation bound
+    |fl(sum) - sum| <= gamma_{M-1} sum|entries|, gamma_j = j u / (1 - j u),
+    u = 2^-24 (M terms summed from 0.0f, the first addition exact)."""
+    flat = G.random_codes(n, m, 600 + n)
+    luts = G.random_floats((nq, m, 16), 601 + nq, 10.0)
+    got = host(bolt.scan_f32(pack_on_gpu(bolt, flat), n, dev(luts))).astype(np.float64)
+    terms = np.stack([luts[:, c, :][:, flat[:, c]] for c in range(m)]).astype(np.float64)  # [M][nq][n]
+    exact = terms.sum(0).T
+    u = 2.0 ** -24
+    gamma = (m - 1) * u / (1 - (m - 1) * u)
+    bound = gamma * np.abs(terms).sum(0).T
+    assert (np.abs(got - exact) <= bound).all()
+    assert (got != exact).any()  # fp32 rounding is really exercised
+
+
 @pytest.mark.parametrize("metric", [0, 1])
 @pytest.mark.parametrize("n,m,nq,k", [(5000, 16, 40, 10), (777, 8, 3, 32), (20, 4, 70, 30), (100_000, 16, 33, 1),
                                       (3, 8, 2, 10)])
@@ -715,6 +765,23 @@ def test_calibrate_gpu_equals_oracle(bolt, orc, cfg_name, metric):
     am = host(am)
     np.testing.assert_array_equal(am[1:], mse_ref)
     assert am[0] == alpha_ref
+    assert host(a)[0] == np.float32(a_ref)
+    np.testing.assert_array_equal(host(b), b_ref.astype(np.float32))
+
+
+def test_calibrate_gpu_alpha_above_zero(bolt, orc):
+    """The tail-heavy tables of the oracle pin (tests/test_oracle_pins.py)
+    where alpha = 0.001 wins: the GPU picks the same alpha, (a, b) and grid
+    errors, bit for bit."""
+    rng = np.random.default_rng(7)
+    D = rng.uniform(0.0, 1.0, (12_500, 2, 16))
+    D[17, 0, 3], D[5, 1, 1] = 256.0, -200.0
+    a_ref, b_ref, alpha_ref, mse_ref = orc.calibrate(D)
+    assert alpha_ref == 0.001
+    a, b, am = bolt.calibrate(dev(D))
+    am = host(am)
+    assert am[0] == alpha_ref
+    np.testing.assert_array_equal(am[1:], mse_ref)
     assert host(a)[0] == np.float32(a_ref)
     np.testing.assert_array_equal(host(b), b_ref.astype(np.float32))
 
