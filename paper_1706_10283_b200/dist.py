@@ -35,6 +35,29 @@ def gather_keys(keys: torch.Tensor, group=None) -> torch.Tensor:
     return out.view(torch.uint64).view((world,) + tuple(keys.shape))
 
 
+def gather_codes(codes: torch.Tensor, n_local: int, m: int, group=None) -> tuple[torch.Tensor, int]:
+    """Every rank's layout-v1 code words -> the whole database's words on every
+    rank, in rank (= row) order, and the total row count.  Shards start on
+    8-row groups (shard_range), so the word ranges concatenate; only the last
+    rank may end in a partial group.  Used to check a sharded result against
+    one device's scan of all rows (bench.py --gpus N)."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    mine = torch.tensor([n_local], dtype=torch.int64, device=codes.device)
+    ns = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(ns, mine, group=group)
+    ns = [int(x.item()) for x in ns]
+    if any(n % 8 for n in ns[:-1]):
+        raise ValueError(f"shards must hold whole 8-row groups except the last: {ns}")
+    words = [-(-n // 8) * m for n in ns]
+    wmax = max(max(words), 1)
+    pad = torch.zeros(wmax, dtype=torch.int32, device=codes.device)
+    pad[:words[rank]] = codes[:words[rank]].view(torch.int32)
+    out = torch.empty(world * wmax, dtype=torch.int32, device=codes.device)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    whole = torch.cat([out[r * wmax:r * wmax + words[r]] for r in range(world)])
+    return whole.view(torch.uint32), sum(ns)
+
+
 def sharded_topk(codes_shard: torch.Tensor, n_shard: int, qluts: torch.Tensor, k: int, metric,
                  index_base: int, group=None, variant: int = 0) -> torch.Tensor:
     """Top-k over the union of all ranks' shards (every rank gets the result)."""

@@ -34,3 +34,6 @@ def test_bench_json_contract(config, extra):
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert "workload" in d["config"]
+    nt = d["near_ties"]  # stage parity of the run's own codes and tables (SURVEY 8(c) rules)
+    assert nt["code_mismatches_not_near_tie"] == 0 and nt["table_mismatches_not_near_tie"] == 0
+    assert d["cpu_baseline"]["cpu"]

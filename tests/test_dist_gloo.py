@@ -103,3 +103,32 @@ def test_query_range_properties():
             rs = [query_range(nq, world, r) for r in range(world)]
             assert rs[0][0] == 0 and rs[-1][1] == nq
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+
+
+def _codes_worker(rank, world, port, n, m, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1706_10283_b200.dist import gather_codes, shard_range
+        words = np.random.default_rng(3).integers(0, 2**32, (n + 7) // 8 * m, dtype=np.uint64).astype(np.uint32)
+        r0, r1 = shard_range(n, world, rank)
+        local = torch.from_numpy(words[r0 // 8 * m:(r1 + 7) // 8 * m].copy())
+        whole, n_all = gather_codes(local, r1 - r0, m)
+        np.save(os.path.join(out_dir, f"c{rank}.npy"), whole.numpy())
+        assert n_all == n
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,world", [(1003, 2), (16, 2), (999, 3)])
+def test_gather_codes_reassembles_database(tmp_path, n, world):
+    """Row shards' layout-v1 words gathered on every rank equal the whole
+    database's words (the exactness check of bench.py --gpus N)."""
+    m = 4
+    port = _free_port()
+    mp.start_processes(_codes_worker, args=(world, port, n, m, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    words = np.random.default_rng(3).integers(0, 2**32, (n + 7) // 8 * m, dtype=np.uint64).astype(np.uint32)
+    for r in range(world):
+        np.testing.assert_array_equal(np.load(tmp_path / f"c{r}.npy"), words)
