@@ -77,9 +77,13 @@ typedef enum {
     BOLT_VARIANT_AUTO = 0,  /* library picks (documented in DESIGN.md) */
     BOLT_VARIANT_PRMT = 1,  /* CUDA-core PRMT byte-permute lookups */
     BOLT_VARIANT_TC = 2,    /* tcgen05 one-hot(codes) x table, kind::i8 */
-    BOLT_VARIANT_TCS = 3    /* tcgen05 with the roles swapped for small query batches:
+    BOLT_VARIANT_TCS = 3,   /* tcgen05 with the roles swapped for small query batches:
                                vectors on the MMA's M side, nq <= 128 queries on N
                                (top-k only, k <= 32, m in {8, 16, 32}) */
+    BOLT_VARIANT_SP = 4     /* tcgen05.mma.sp (2:4 structured-sparse A = the one-hot
+                               codes, compressed): vectors on M, 224
+                               queries per tile on N; twice the dense int8 rate
+                               (top-k only, m in {8, 16, 32}, k <= 32; k <= 16 for m = 32) */
 } bolt_variant;
 
 /* ------------------------------------------------------------------ info */

@@ -19,7 +19,7 @@ from . import _lib
 from ._lib import BoltError  # noqa: F401
 
 L2SQ, DOT = 0, 1
-VARIANT_AUTO, VARIANT_PRMT, VARIANT_TC, VARIANT_TCS = 0, 1, 2, 3
+VARIANT_AUTO, VARIANT_PRMT, VARIANT_TC, VARIANT_TCS, VARIANT_SP = 0, 1, 2, 3, 4
 K = 16
 _METRICS = {"l2": L2SQ, "l2sq": L2SQ, "euclidean": L2SQ, "dot": DOT, "mips": DOT}
 
@@ -197,11 +197,11 @@ def topk_workspace_bytes(n: int, m: int, nq: int, k: int, variant: int = VARIANT
 
 
 def topk_plan(n: int, m: int, nq: int, k: int, variant: int = VARIANT_AUTO):
-    """-> (resolved variant name 'prmt' | 'tc' | 'tcs', number of merged row partitions)."""
+    """-> (resolved variant name 'prmt' | 'tc' | 'tcs' | 'sp', number of merged row partitions)."""
     import ctypes
     v, p = ctypes.c_int(0), ctypes.c_int(0)
     _lib.call("bolt_topk_plan", n, m, nq, k, variant, ctypes.byref(v), ctypes.byref(p))
-    return {VARIANT_PRMT: "prmt", VARIANT_TC: "tc", VARIANT_TCS: "tcs"}[v.value], p.value
+    return {VARIANT_PRMT: "prmt", VARIANT_TC: "tc", VARIANT_TCS: "tcs", VARIANT_SP: "sp"}[v.value], p.value
 
 
 def topk(codes: torch.Tensor, n: int, qluts: torch.Tensor, k: int, metric, index_base: int = 0,

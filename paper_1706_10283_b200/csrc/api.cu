@@ -111,16 +111,18 @@ TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     p.small = v == BOLT_VARIANT_PRMT && topk_small_supported(n, m, nq, k);
     p.parts = v == BOLT_VARIANT_TC    ? topk_tc_parts(n, m, nq, k, sms)
               : v == BOLT_VARIANT_TCS ? topk_tcs_parts(n, m, nq, k, sms)
+              : v == BOLT_VARIANT_SP  ? topk_sp_parts(n, m, nq, k, sms)
               : p.small               ? topk_small_parts(n, m, nq, k, sms)
                                       : topk_prmt_parts(n, m, nq, k, sms);
     p.klist = v == BOLT_VARIANT_TC && k > kTcListMax ? kTcListMax : k;
-    p.ws = p.parts > 1 || p.small || v == BOLT_VARIANT_TCS ? (size_t)p.parts * nq * p.klist * sizeof(uint64_t) : 0;
+    p.ws = p.parts > 1 || p.small || v == BOLT_VARIANT_TCS || v == BOLT_VARIANT_SP
+               ? (size_t)p.parts * nq * p.klist * sizeof(uint64_t) : 0;
     // shared per-query thresholds (u32) after the partial lists: PRMT one word,
     // TC 3 nq + 1 (k-th value words + 8 B aligned half-list pairs, scan_tc.cu),
     // small-batch PRMT 33 nq (k-th value word + 32 minima slots, scan_small.cu)
     if (p.ws > 0)
         p.ws += (size_t)(v == BOLT_VARIANT_TC ? (k > kTcListMax ? 4 * nq : 3 * nq + 1) : p.small ? 33 * nq : nq) *
-                sizeof(uint32_t);  // TCS: nq words
+                sizeof(uint32_t);  // TCS, SP: nq words
     if (v == BOLT_VARIANT_TC && k > kTcListMax) {
         // flags [nq] u32, count, then the exact fallback for flagged queries in
         // batches of kFallbackBatch: gathered tables, keys, small-batch workspace
@@ -410,7 +412,7 @@ bolt_status bolt_topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int
                            int* parts) {
     TRY(check_m(m));
     if (n < 0 || nq < 0 || k < 1 || k > kMaxK) return fail(BOLT_E_SHAPE, "bad n/nq/k");
-    if (variant < BOLT_VARIANT_AUTO || variant > BOLT_VARIANT_TCS) return fail(BOLT_E_RANGE, "variant %d", variant);
+    if (variant < BOLT_VARIANT_AUTO || variant > BOLT_VARIANT_SP) return fail(BOLT_E_RANGE, "variant %d", variant);
     TopkPlan p = topk_plan(n, m, nq, k, variant, sms_or_default());
     if (resolved_variant) *resolved_variant = p.variant;
     if (parts) *parts = p.parts;
@@ -428,7 +430,7 @@ bolt_status bolt_topk_ex(const uint32_t* codes, int64_t n, int m, const uint8_t*
     TRY(scan_common(codes, n, m, qluts, nq));
     if (k < 1 || k > kMaxK) return fail(BOLT_E_SHAPE, "k = %d outside 1..128", k);
     if (metric != BOLT_L2SQ && metric != BOLT_DOT) return fail(BOLT_E_RANGE, "metric %d", (int)metric);
-    if (variant < BOLT_VARIANT_AUTO || variant > BOLT_VARIANT_TCS) return fail(BOLT_E_RANGE, "variant %d", variant);
+    if (variant < BOLT_VARIANT_AUTO || variant > BOLT_VARIANT_SP) return fail(BOLT_E_RANGE, "variant %d", variant);
     if (index_base < 0 || index_base + n >= (int64_t(1) << 48))
         return fail(BOLT_E_RANGE, "index_base + n must be < 2^48");
     if (nq == 0) return BOLT_OK;
@@ -442,6 +444,8 @@ bolt_status bolt_topk_ex(const uint32_t* codes, int64_t n, int m, const uint8_t*
         return fail(BOLT_E_RANGE, "tcgen05 variant does not support m=%d k=%d", m, k);
     if (variant == BOLT_VARIANT_TCS && !topk_tcs_supported(n, m, nq, k))
         return fail(BOLT_E_RANGE, "swapped tcgen05 variant needs m in {8,16,32}, nq <= 128, k <= 32");
+    if (variant == BOLT_VARIANT_SP && !topk_sp_supported(n, m, nq, k))
+        return fail(BOLT_E_RANGE, "sparse tcgen05 variant needs m in {8,16,32}, k <= 32 (k <= 16 for m = 32)");
     TopkPlan p = topk_plan(n, m, nq, k, variant, d.sms);
     if (p.ws > 0 && (!ws || ws_bytes < p.ws))
         return fail(BOLT_E_WORKSPACE, "workspace of %zu bytes required, %zu given", p.ws, ws_bytes);
@@ -449,6 +453,11 @@ bolt_status bolt_topk_ex(const uint32_t* codes, int64_t n, int m, const uint8_t*
     ScanArgs a{codes, n, ceil_div(n, 8), m, qluts, nq};
     uint64_t* parts_out = p.parts > 1 ? static_cast<uint64_t*>(ws) : out_keys;
     cudaError_t e = cudaSuccess;
+    if (p.variant == BOLT_VARIANT_SP) {
+        e = launch_topk_sp(a, k, metric, index_base, p.parts, parts_out, s);
+        if (e != cudaSuccess) return cuda_status(e, "bolt_topk scan");
+        return cuda_status(launch_merge_many(parts_out, p.parts, nq, k, k, out_keys, s), "bolt_topk merge");
+    }
     if (p.variant == BOLT_VARIANT_TCS) {
         e = launch_topk_tcs(a, k, metric, index_base, p.parts, parts_out, s);
         if (e != cudaSuccess) return cuda_status(e, "bolt_topk scan");

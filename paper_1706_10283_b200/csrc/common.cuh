@@ -136,6 +136,11 @@ int topk_tcs_supported(int64_t n, int m, int64_t nq, int k);
 int topk_tcs_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
 cudaError_t launch_topk_tcs(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
                             uint64_t* part_keys, cudaStream_t s);
+// 2:4-sparse tcgen05 top-k (scan_sp.cu): vectors on M, 224 queries per tile
+int topk_sp_supported(int64_t n, int m, int64_t nq, int k);
+int topk_sp_parts(int64_t n, int m, int64_t nq, int k, int num_sms);
+cudaError_t launch_topk_sp(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
+                           uint64_t* part_keys, cudaStream_t s);
 // part_keys: parts*nq*k keys followed by the shared threshold words (zeroed by the launch)
 cudaError_t launch_topk_tc(const ScanArgs& a, int k, int metric, int64_t index_base, int parts,
                            uint64_t* part_keys, int sms, cudaStream_t s);

@@ -272,6 +272,38 @@ def test_topk_tc_bitexact(bolt, orc, metric, n, m, nq, k, hi, base):
     np.testing.assert_array_equal(got, ref)
 
 
+# 2:4-sparse tcgen05 (f2): vectors on M (compressed one-hot + TMEM metadata),
+# 224 queries per tile on N; k <= 32 (k <= 16 for m = 32)
+SP_CASES = [
+    # n, m, nq, k, lut_hi, index_base
+    (1, 16, 1, 1, 256, 0),
+    (5, 8, 3, 10, 256, 0),              # k > n: padding
+    (300, 16, 225, 10, 4, 7),           # two query tiles, heavy ties, ragged tile
+    (4097, 16, 33, 10, 16, 0),
+    (2500, 8, 200, 32, 8, 123456),
+    (3000, 32, 7, 16, 256, 0),
+    (65537, 16, 449, 10, 8, 0),         # several row partitions + tail, three query tiles
+    (20000, 32, 64, 12, 256, 2**40),
+    (20000, 16, 230, 32, 256, 2**40),
+    (100000, 16, 700, 10, 256, 0),
+    (1_000_000, 16, 300, 10, 256, 5),
+    (777, 8, 24, 4, 3, 0),
+    (1_000_003, 32, 250, 10, 256, 0),
+]
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+@pytest.mark.parametrize("n,m,nq,k,hi,base", SP_CASES)
+def test_topk_sp_bitexact(bolt, orc, metric, n, m, nq, k, hi, base):
+    """Sparse one-hot x table contraction: same integers, same keys."""
+    flat = G.random_codes(n, m, n + m + k + 3)
+    ql = G.random_qluts(nq, m, nq + k + 3, hi=hi)
+    ref = orc.topk(flat, ql, k, metric, index_base=base)
+    got = host(bolt.topk(pack_on_gpu(bolt, flat), n, dev(ql), k, metric, index_base=base,
+                         variant=bolt.VARIANT_SP))
+    np.testing.assert_array_equal(got, ref)
+
+
 # 32 < k <= 128 on the tensor cores: lists of 32 merged, verified, and the
 # flagged queries redone exactly (the constant-table and few-partition cases
 # force the fallback; the large random case mostly does not)

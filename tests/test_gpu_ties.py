@@ -60,10 +60,11 @@ def rows_of_levels(levels, m):
     return np.repeat(np.asarray(levels, np.uint8)[:, None], m, axis=1)
 
 
-def _check(bolt, orc, flat, ql, k, metric, nq_mode, index_base=0):
+def _check(bolt, orc, flat, ql, k, metric, nq_mode, index_base=0, variant=None):
     n = flat.shape[0]
     codes = bolt.pack_codes(dev(flat))
-    got = host(bolt.topk(codes, n, dev(ql), k, metric, index_base=index_base, variant=bolt.VARIANT_TC))
+    variant = bolt.VARIANT_TC if variant is None else variant
+    got = host(bolt.topk(codes, n, dev(ql), k, metric, index_base=index_base, variant=variant))
     ref = orc.topk(flat, ql, k, metric, index_base=index_base)
     np.testing.assert_array_equal(got, ref, err_msg=f"mode {nq_mode}, k {k}, metric {metric}")
     return got
@@ -129,3 +130,33 @@ def test_binary_tables_random_codes(bolt, orc, metric, m):
     for nq, k in ((100, 10), (300, 32), (150, 100)):
         ql = G.random_qluts(nq, m, 41 + nq, hi=2)
         _check(bolt, orc, flat, ql, k, metric, f"nq={nq}")
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+@pytest.mark.parametrize("k", [1, 10, 16, 32])
+@pytest.mark.parametrize("nq", [1, 224, 300])
+@pytest.mark.parametrize("n", [256, 3001, 70_001])
+def test_three_level_ties_sparse(bolt, orc, metric, k, nq, n):
+    """The same tie patterns through the 2:4-sparse kernel (BOLT_VARIANT_SP),
+    whose lists take candidates in vector order per query."""
+    m = 16
+    levels = np.random.default_rng(n + k).integers(0, 3, n)
+    flat = rows_of_levels(levels, m)
+    ql = three_level_tables(nq, m, metric)
+    got = _check(bolt, orc, flat, ql, k, metric, "sp", index_base=11, variant=bolt.VARIANT_SP)
+    best = np.flatnonzero(levels == 1)[:k] + 11
+    _, idx = bolt.keys_split(dev(got), metric)
+    np.testing.assert_array_equal(host(idx)[0, :len(best)], best)
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+@pytest.mark.parametrize("m,k", [(8, 32), (16, 10), (32, 16)])
+def test_constant_and_binary_tables_sparse(bolt, orc, metric, m, k):
+    n = 50_001
+    flat = G.random_codes(n, m, 5 + m)
+    ql = np.full((250, m, 16), 7, np.uint8)
+    got = _check(bolt, orc, flat, ql, k, metric, "sp", variant=bolt.VARIANT_SP)
+    _, idx = bolt.keys_split(dev(got), metric)
+    assert (host(idx) == np.arange(k)[None]).all()
+    ql = G.random_qluts(230, m, 41 + m, hi=2)
+    _check(bolt, orc, flat, ql, k, metric, "sp", variant=bolt.VARIANT_SP)

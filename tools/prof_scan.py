@@ -42,7 +42,8 @@ else:
     codes = bolt.pack_codes(torch.from_numpy(G.random_codes(a.n, a.m, 1)).to(dev))
     ql = torch.from_numpy(G.random_qluts(a.nq, a.m, 2)).to(dev)
     metric = 0
-v = {"prmt": bolt.VARIANT_PRMT, "tc": bolt.VARIANT_TC, "tcs": bolt.VARIANT_TCS, "auto": bolt.VARIANT_AUTO}[a.variant]
+v = {"prmt": bolt.VARIANT_PRMT, "tc": bolt.VARIANT_TC, "tcs": bolt.VARIANT_TCS, "sp": bolt.VARIANT_SP,
+     "auto": bolt.VARIANT_AUTO}[a.variant]
 if a.what == "encode":
     X = torch.from_numpy(G.database(G.CONFIGS["c2"], a.n)).to(dev)
     C = torch.from_numpy(G.random_floats((a.m, 16, 128 // a.m), 3, 50.0) + 100).to(dev)
@@ -97,7 +98,10 @@ if os.environ.get("BOLT_COUNTERS"):
     bolt._lib.load().bolt_debug_counters(ctypes.cast(buf, ctypes.c_void_p), 24)
     names = ["prod_wait_empty", "epi_wait_tfull", "epi_wait+load", "mma_wait_full", "mma_wait_tempty",
              "tiles(leader)", "cta_cycles", "ctas", "epi_proc_cycles", "slow_entries", "inserts",
-             "warp_slow_chunks", "wslow_t<8", "wslow_t<64", "wslow_t<256", "wslow_t>=256", "warp_cand_iters", "lanes_no_thr_t>=1", "sum_thr_t1"]
+             "warp_slow_chunks", "wslow_t<8", "wslow_t<64", "wslow_t<256", "wslow_t>=256", "warp_cand_iters", "lanes_no_thr_t>=1", "sum_thr_t1", "-", "-", "-", "-", "-"]
+    if a.variant == "sp":
+        names = names[:16] + ["sp_group_entries", "sp_query_entries", "sp_candidates", "sp_list_changes",
+                              "sp_warp_tiles", "sp_groups_t<16", "sp_groups_t<128", "sp_groups_t>=128"]
     tiles = max(buf[5], 1)
     ctas = max(buf[7], 1)
     print("counters:", {n: int(buf[i]) for i, n in enumerate(names)})
