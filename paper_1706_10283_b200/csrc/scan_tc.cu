@@ -99,6 +99,7 @@ constexpr int kPrefetch = 3;             // tiles of code words in flight per pr
 // 128-byte block per warp (4 KB)
 constexpr int kScratchStrideTopk = 20;
 constexpr int kScratchStrideFull = 32;
+constexpr int kStorePieces = 2;          // full output: TMA stores per 32-row x 128-byte warp block
 
 // QROWS: query rows of the table buffer per CTA (kQM, or kNQ/2 in the
 // swapped top-k); LIST_BYTES: the swapped top-k's per-warp lists (else the
@@ -640,7 +641,9 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                 constexpr int kSeg = 8 * kQPU;          // queries per 128-byte segment
 #pragma unroll
                 for (int sg = 0; sg < kCols / kSeg; ++sg) {
-                    // this lane's row: 8 units of the segment
+                    // this lane's row: 8 units of the segment, computed before the
+                    // staging block is reclaimed (overlaps the previous stores' reads)
+                    uint4 us[8];
 #pragma unroll
                     for (int f = 0; f < 8; ++f) {
                         uint4 u;
@@ -659,22 +662,35 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                             u = make_uint4(__float_as_uint(fv[0]), __float_as_uint(fv[1]), __float_as_uint(fv[2]),
                                            __float_as_uint(fv[3]));
                         }
-                        stg[lane * 8 + (f ^ (lane & 7))] = u;
+                        us[f] = u;
                     }
                     if (fo.tma) {
-                        // one TMA store of the warp's 32 x 128-byte block (the staging
-                        // layout is the tensor map's 128-byte swizzle)
-                        fence_proxy_async();
-                        __syncwarp();
-                        if (lane == 0) {
-                            tma_store_2d(&omap, smem_u32(stg), (int)(qb + sg * kSeg), (int)vrow0);
-                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                            // the staging block is rewritten by the next segment
-                            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        // kStorePieces TMA stores per segment, one per row slice of the
+                        // warp's 32 x 128-byte block (the staging layout is the tensor
+                        // map's 128-byte swizzle): a slice is rewritten only once its
+                        // store of the previous segment has been read (wait_group.read
+                        // kStorePieces - 1), so stores stay in flight while the next
+                        // slice is staged
+#pragma unroll
+                        for (int hh = 0; hh < kStorePieces; ++hh) {
+                            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStorePieces - 1) : "memory");
+                            __syncwarp();
+                            if (lane / (32 / kStorePieces) == hh) {
+#pragma unroll
+                                for (int f = 0; f < 8; ++f) stg[lane * 8 + (f ^ (lane & 7))] = us[f];
+                            }
+                            fence_proxy_async();
+                            __syncwarp();
+                            if (lane == 0) {
+                                tma_store_2d(&omap, smem_u32(stg + hh * (256 / kStorePieces)), (int)(qb + sg * kSeg),
+                                             (int)(vrow0 + (32 / kStorePieces) * hh));
+                                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                            }
                         }
-                        __syncwarp();
                         continue;
                     }
+#pragma unroll
+                    for (int f = 0; f < 8; ++f) stg[lane * 8 + (f ^ (lane & 7))] = us[f];
                     __syncwarp();
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
@@ -1028,7 +1044,7 @@ cudaError_t launch_scan_tc(const ScanArgs& a, uint16_t* out16, float* out32, int
     if (vec && tc::encode_tiled()) {
         const cuuint64_t dims[2] = {(cuuint64_t)a.nq, (cuuint64_t)a.n};
         const cuuint64_t strides[1] = {(cuuint64_t)(ldo * esz)};
-        const cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 32u};
+        const cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)(32 / tc::kStorePieces)};  // a row slice of a warp's block
         const cuuint32_t estr[2] = {1u, 1u};
         tma = tc::encode_tiled()(&omap, out32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, out,
                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
