@@ -59,15 +59,22 @@ def codes_words(n: int, m: int) -> int:
 
 
 # ------------------------------------------------------------------ h (encode)
-def encode(X: torch.Tensor, C: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-    """X fp32 [n][J], C fp32 [M][16][J/M] -> layout-v1 codes, uint32 [ceil(n/8)*M]."""
+ENCODE_AUTO, ENCODE_DIRECT, ENCODE_EXPANDED = 0, 1, 2
+
+
+def encode(X: torch.Tensor, C: torch.Tensor, out: torch.Tensor | None = None,
+           variant: int = ENCODE_AUTO) -> torch.Tensor:
+    """X fp32 [n][J], C fp32 [M][16][J/M] -> layout-v1 codes, uint32 [ceil(n/8)*M].
+    variant: ENCODE_AUTO / ENCODE_DIRECT (direct differences) or ENCODE_EXPANDED
+    (expanded distances + exact fallback); all return the same codes bit for bit."""
     _cuda(X, "X", torch.float32)
     _cuda(C, "C", torch.float32)
     n, j = X.shape
     m = C.shape[0]
     if out is None:
         out = torch.empty(codes_words(n, m), dtype=torch.uint32, device=X.device)
-    _lib.call("bolt_encode", X.data_ptr(), n, j, j, C.data_ptr(), m, out.data_ptr(), _stream(X.device))
+    _lib.call("bolt_encode_ex", X.data_ptr(), n, j, j, C.data_ptr(), m, out.data_ptr(), int(variant),
+              _stream(X.device))
     return out
 
 

@@ -24,6 +24,7 @@ SIGNATURES = {
     "bolt_last_error": ([], ctypes.c_char_p),
     "bolt_codes_words": ([_I64, _I32], _I64),
     "bolt_encode": ([_P, _I64, _I32, _I64, _P, _I32, _P, _P], _I32),
+    "bolt_encode_ex": ([_P, _I64, _I32, _I64, _P, _I32, _P, _I32, _P], _I32),
     "bolt_encode_append": ([_P, _I64, _I32, _I64, _P, _I32, _P, _I64, _P], _I32),
     "bolt_pack_codes": ([_P, _I64, _I32, _P, _P], _I32),
     "bolt_unpack_codes": ([_P, _I64, _I32, _P, _P], _I32),

@@ -160,6 +160,13 @@ int64_t bolt_codes_words(int64_t n, int m) {
 
 bolt_status bolt_encode(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,
                         uint32_t* codes, bolt_stream_t stream) {
+    return bolt_encode_ex(X, n, j, ldx, C, m, codes, BOLT_ENCODE_AUTO, stream);
+}
+
+bolt_status bolt_encode_ex(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,
+                           uint32_t* codes, int variant, bolt_stream_t stream) {
+    if (variant != BOLT_ENCODE_AUTO && variant != BOLT_ENCODE_DIRECT && variant != BOLT_ENCODE_EXPANDED)
+        return fail(BOLT_E_RANGE, "encode variant %d", variant);
     TRY(check_jm(j, m));
     if (n < 0) return fail(BOLT_E_SHAPE, "n = %lld < 0", (long long)n);
     if (ldx < j) return fail(BOLT_E_SHAPE, "ldx = %lld < j = %d", (long long)ldx, j);
@@ -169,7 +176,9 @@ bolt_status bolt_encode(const float* X, int64_t n, int j, int64_t ldx, const flo
     if (!aligned(C, 16)) return fail(BOLT_E_ALIGN, "bolt_encode: C must be 16-byte aligned");
     DevInfo d;
     TRY(device_info(&d));
-    return cuda_status(launch_encode(X, n, j, ldx, C, m, codes, d.sms, (cudaStream_t)stream), "bolt_encode");
+    return cuda_status(launch_encode(X, n, j, ldx, C, m, codes, d.sms, (cudaStream_t)stream,
+                                     variant != BOLT_ENCODE_EXPANDED),
+                       "bolt_encode");
 }
 
 // ---- Bolt No Quantize (scan_f32.cu)

@@ -58,6 +58,7 @@ def test_host_validation(lib):
     assert lib.bolt_encode(None, 10, 32, 16, None, 8, None, None) == E_SHAPE
     assert lib.bolt_encode(None, 10, 32, 32, None, 8, None, None) == E_NULL
     assert lib.bolt_encode(None, 0, 32, 32, None, 8, None, None) == 0  # empty is a no-op
+    assert lib.bolt_encode_ex(None, 10, 32, 32, None, 8, None, 7, None) == 3  # BOLT_E_RANGE: unknown variant
     assert lib.bolt_quantize_luts(None, 4, 8, ctypes.c_float(0.0), None, None, None) == E_RANGE
     assert lib.bolt_scan(None, 10, 8, None, 4, None, 2, None) == E_NULL
     assert lib.bolt_topk_ex(None, 10, 8, None, 4, 0, 0, 0, None, None, 0, 0, None) == E_NULL

@@ -80,6 +80,33 @@ def test_encode_centroid_identity(bolt, orc):
     np.testing.assert_array_equal(got, idx)
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_encode_fast_equals_direct_near_ties(bolt, orc, seed):
+    """The expanded-distance encoder (ENCODE_EXPANDED: ||c||^2 - 2 x.c ranking,
+    rounding bound, direct fallback) returns the direct-difference kernel's
+    codes bit for bit, on rows built at or near midpoints of centroid pairs
+    (exact fp32 ties, 1e-5 .. 0.5 offsets) with c2-sized coordinates (0..255,
+    where the expansion's rounding is largest), duplicated centroids and rows
+    equal to centroids; and both agree with the oracle up to near-ties."""
+    m, L, n = 16, 8, 60_000
+    rng = np.random.default_rng(seed)
+    C = rng.uniform(0, 255, (m, 16, L)).astype(np.float32)
+    C[:4, 9] = C[:4, 4]                       # exact duplicate centroids in 4 codebooks
+    a = rng.integers(0, 16, (n, m))
+    b = rng.integers(0, 16, (n, m))
+    mid = (C[np.arange(m)[None, :], a] + C[np.arange(m)[None, :], b]) / np.float32(2)
+    scale = rng.choice(np.array([0, 0, 1e-5, 1e-3, 0.5], np.float32), size=(n, m, 1))
+    X = (mid + scale * rng.standard_normal((n, m, L)).astype(np.float32)).astype(np.float32)
+    X[: n // 10] = C[np.arange(m)[None, :], a[: n // 10]]  # rows on centroids
+    X = np.ascontiguousarray(X.reshape(n, m * L))
+    Xd, Cd = dev(X), dev(C)
+    fast = host(bolt.encode(Xd, Cd, variant=bolt.ENCODE_EXPANDED))
+    direct = host(bolt.encode(Xd, Cd, variant=bolt.ENCODE_DIRECT))
+    np.testing.assert_array_equal(host(bolt.encode(Xd, Cd)), direct)
+    np.testing.assert_array_equal(fast, direct)
+    _encode_check(bolt, orc, X[:5000], C)
+
+
 # ------------------------------------------------------------------------ LUT
 @pytest.mark.parametrize("metric", [0, 1])
 @pytest.mark.parametrize("nq,m,L", [(1, 1, 1), (16, 8, 4), (33, 16, 8), (7, 32, 16), (5, 64, 3)])

@@ -22,6 +22,7 @@ p.add_argument("--variant", default="prmt")
 p.add_argument("--what", default="topk")
 p.add_argument("--reps", type=int, default=2)
 p.add_argument("--prefill", action="store_true")
+p.add_argument("--direct", action="store_true", help="encode: the direct-difference kernel (else the expanded one)")
 p.add_argument("--config", default="", help="use a BASELINE config's real pipeline data (c2, c3)")
 a = p.parse_args()
 dev = torch.device("cuda")
@@ -45,8 +46,12 @@ else:
 v = {"prmt": bolt.VARIANT_PRMT, "tc": bolt.VARIANT_TC, "tcs": bolt.VARIANT_TCS, "sp": bolt.VARIANT_SP,
      "auto": bolt.VARIANT_AUTO}[a.variant]
 if a.what == "encode":
-    X = torch.from_numpy(G.database(G.CONFIGS["c2"], a.n)).to(dev)
-    C = torch.from_numpy(G.random_floats((a.m, 16, 128 // a.m), 3, 50.0) + 100).to(dev)
+    if a.config:  # the bench's database and GPU-fitted codebooks
+        X = torch.from_numpy(G.database(cfg, a.n)).to(dev)
+        C = model.C
+    else:
+        X = torch.from_numpy(G.database(G.CONFIGS["c2"], a.n)).to(dev)
+        C = torch.from_numpy(G.random_floats((a.m, 16, 128 // a.m), 3, 50.0) + 100).to(dev)
 full_out = None
 if a.what in ("full", "dequant"):
     full_out = torch.empty((a.n, a.nq), dtype=torch.uint16 if a.what == "full" else torch.float32, device=dev)
@@ -74,7 +79,7 @@ def once():
     elif a.what == "dequant":
         bolt.scan_dequant(codes, a.n, ql, 0.5, 1.0, out=full_out, variant=v)
     elif a.what == "encode":
-        bolt.encode(X, C)
+        bolt.encode(X, C, variant=bolt.ENCODE_DIRECT if a.direct else bolt.ENCODE_EXPANDED)
 
 
 for _ in range(a.reps):
