@@ -99,6 +99,10 @@ constexpr int kPrefetch = 3;             // tiles of code words in flight per pr
 // 128-byte block per warp (4 KB)
 constexpr int kScratchStrideTopk = 20;
 constexpr int kScratchStrideFull = 32;
+constexpr int kUnionParts = 8;           // top-k: finished partitions whose lists seed a unit's bound
+constexpr int kUnionMinTiles = 256;      // ... only for units this long (the read costs ~50 tiles' time)
+constexpr int kUnionGroups = 2;          // top-k: groups of lists of the union bound (epilogue; 5 measured no better)
+static_assert(kUnionGroups == 2 || kUnionGroups == 5, "2 or 5 union groups (load widths)");
 constexpr int kStorePieces = 2;          // full output: TMA stores per 32-row x 128-byte warp block
 
 // QROWS: query rows of the table buffer per CTA (kQM, or kNQ/2 in the
@@ -562,20 +566,26 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
         // value can reach the global top-k only if kv' < own and kv' <= T.
         uint32_t own = kNotFull;
         uint32_t published = kNotFull;
-        // Half-list bound: the ceil(k/2)-th value of this list.  The lists of
-        // the two column halves cover disjoint vectors, so if the best half-0
-        // list and the best half-1 list each hold ceil(k/2) values <= x, the
-        // union holds >= k of them: T2 = max over the two halves of the
-        // per-half minimum of that value is also a valid threshold.  Kept in
-        // two more inverted words per query (gthr_inv[hoff + 2q + half], hoff =
-        // nq rounded up to even).
-        const int hpos = KMAX - 1 - k / 2;
-        uint32_t published_h = k > 1 ? kNotFull : 0u;
+        // Union bound over G = min(k, kUnionGroups) groups of lists: the lists
+        // of a query (id 2 part + half, all disjoint vectors) are dealt into G
+        // groups by id mod G; each publishes its j-th value, j = ceil(k / G),
+        // into its group's word (minimum).  If every group's best list holds
+        // j values <= x, the union holds >= G j >= k of them, so the largest
+        // group minimum is a valid threshold.  G = 2 (the column halves, j =
+        // ceil(k/2)); G = 5 (j = 2 at k = 10), better in an order-statistics
+        // simulation, measured no fewer slow-path entries on c2 and a slower
+        // scan.  Inverted words gthr_inv[hoff + 8q + g], hoff =
+        // nq rounded up to a multiple of 4.
+        const int hG = k < kUnionGroups ? k : kUnionGroups;
+        const int hj = (k + hG - 1) / hG;
+        const int hpos = KMAX - k + hj - 1;
+        const int hgrp = (2 * part + half) % hG;
+        uint32_t published_h = hG > 1 ? kNotFull : 0u;
         bool changed = false;  // list changed since the half bound was last published
         const bool qvalid = q0 + q < a.nq;
         uint32_t* gq = gthr_inv + (qvalid ? q0 + q : 0);
         uint32_t thr = kNotFull;
-        uint32_t* gh = gthr_inv + ((a.nq + 1) & ~int64_t(1)) + 2 * (qvalid ? q0 + q : 0);  // 8 B aligned
+        uint32_t* gh = gthr_inv + ((a.nq + 3) & ~int64_t(3)) + 8 * (qvalid ? q0 + q : 0);  // 16 B aligned
         // kGroup (lists of 32 for a final k <= 32 G, G = a.noshare): a list's
         // 32nd value bounds only 32 values, so the lists of a query are dealt
         // into G groups (list id mod G) and each group keeps the minimum of its
@@ -586,11 +596,57 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
         const int ngrp = kGroup ? a.noshare : 0;  // compile-time 0 outside the large-k instantiations
         uint32_t* gg = gthr_inv + 4 * (qvalid ? q0 + q : 0);
         const int grp = kGroup ? (2 * part + half) % ngrp : 0;
-        uint32_t g_next = 0, gh0 = 0, gh1 = 0;  // inverted shared thresholds (0 = none yet), fetched a tile ahead
+        uint32_t g_next = 0;                    // inverted shared threshold (0 = none yet), fetched a tile ahead
+        uint32_t gw[kUnionGroups] = {};         // inverted union-group words, fetched a tile ahead
         uint32_t gs[4] = {0u, 0u, 0u, 0u};      // group words (kGroup)
+        auto load_union = [&]() {
+            if constexpr (kUnionGroups == 2) {
+                asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gw[0]), "=r"(gw[1]) : "l"(gh));
+            } else {
+                asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(gw[0]), "=r"(gw[1]), "=r"(gw[2]), "=r"(gw[3])
+                             : "l"(gh));
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gw[4]) : "l"(gh + 4));
+            }
+        };
+        // Finished partitions' lists (done[p][tq] == number of CTAs of a
+        // unit): their keys are final, every entry is a distinct row, so the
+        // k-th smallest value of their union bounds this query's k-th best --
+        // for units of later waves, the exact k-th of 20-80 % of the rows,
+        // much tighter than any single list's k-th.  Read once, at unit start.
+        // (c2: scan 1.78 -> 1.73 ms)
+        uint32_t* done = gthr_inv + ((a.nq + 3) & ~int64_t(3)) + 8 * a.nq;  // [rparts][tiles_q]
+        if (share && kOut == 0 && qvalid && part > 0 && ntiles >= kUnionMinTiles) {
+            RegList<KMAX> ul;
+            ul.init(k);
+            // the first kUnionParts partitions (they finish first); any subset of
+            // finished lists bounds, and more than 16 lists cost more to read
+            // than they tighten (c3's 80 partitions: 0.33 -> 0.53 ms reading all)
+            for (int pp = 0; pp < min(part, kUnionParts); ++pp) {
+                uint32_t dn;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(dn) : "l"(done + (int64_t)pp * tiles_q + tq));
+                if (dn != (kPairT ? 2u : 1u)) continue;
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const uint64_t* src = part_keys + ((int64_t)(2 * pp + hh) * a.nq + q0 + q) * k;
+                    for (int i = 0; i < k; ++i) {
+                        const uint64_t key = src[i];
+                        if (key == ~0ull) break;
+                        const uint32_t kv64 = (uint32_t)(key >> 48);
+                        const uint32_t kvp = kDot ? C::KVMAX - (0xFFFFu - kv64) : kv64;
+                        if (kvp + 1u >= ul.v[KMAX - 1]) break;  // sorted list: the rest is no better
+                        ul.insert(kvp + 1u);  // + 1: value 0 must not meet the 0 padding slots
+                    }
+                }
+            }
+            if (ul.v[KMAX - 1] != 0xFFFFFFFFu) {
+                const uint32_t tu = ul.v[KMAX - 1] - 1u;  // k-th smallest value of the union
+                asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gq), "r"(0xFFFFu - tu) : "memory");
+            }
+        }
         if (share) {
             asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g_next) : "l"(gq));
-            asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gh0), "=r"(gh1) : "l"(gh));
+            load_union();
         }
         const uint32_t tlane = (uint32_t)(quad * 32) << 16;
         for (int tile = 0; tile < ntiles; ++tile) {
@@ -728,12 +784,15 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                 asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gs[0]), "=r"(gs[1]) : "l"(gg));
                 asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gs[2]), "=r"(gs[3]) : "l"(gg + 2));
             }
-            thr = min(min(own, 0xFFFFu - g_next + 1u), 0xFFFFu - min(gh0, gh1) + 1u);
+            uint32_t hmin = gw[0];  // groups >= hG hold no list: they do not bound (treated as 0xFFFF)
+#pragma unroll
+            for (int g = 1; g < kUnionGroups; ++g) hmin = min(hmin, g < hG ? gw[g] : 0xFFFFu);
+            thr = min(min(own, 0xFFFFu - g_next + 1u), 0xFFFFu - hmin + 1u);
             if (tile >= 1 && thr > 0xFFFFu) BOLT_PROF_WARP(17, 1);  // lanes without a threshold after tile 0
             if (tile == 1) BOLT_PROF_ADD(18, thr);
             if (share) {
                 asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g_next) : "l"(gq));
-                asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(gh0), "=r"(gh1) : "l"(gh));
+                load_union();
             }
             const int tbl = tile * C::N;  // local index of the tile's first vector
             const int nvalid = (int)min64(C::N, vend - vbeg - tbl);
@@ -815,9 +874,9 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             if (changed && qvalid && share) {
                 changed = false;
                 const uint32_t own_h = list.value_at(hpos, C::IDX_BITS);
-                if (own_h < published_h) {  // published_h = 0 for k == 1 (the half bound is own)
+                if (own_h < published_h) {  // published_h = 0 for k == 1 (the union bound is own)
                     published_h = own_h;
-                    asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gh + half), "r"(0xFFFFu - own_h)
+                    asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gh + hgrp), "r"(0xFFFFu - own_h)
                                  : "memory");
                 }
             }
@@ -838,6 +897,15 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                     }
                     dst[i - (KMAX - k)] = out;
                 }
+            }
+        }
+        if (kOut == 0 && share) {
+            // this CTA's lists are written: count it in done[part][tq] (release)
+            asm volatile("bar.sync 1, %0;" ::"n"(kEpilogue) : "memory");
+            if (threadIdx.x == 0) {
+                __threadfence();
+                uint32_t* done = gthr_inv + ((a.nq + 3) & ~int64_t(3)) + 8 * a.nq;
+                atomicAdd(done + (int64_t)part * tiles_q + tq, 1u);
             }
         }
       }
@@ -933,7 +1001,7 @@ cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, 
 #ifdef BOLT_XMODE
     if (const char* x = getenv("BOLT_TC_XMODE")) xmode = atoi(x);
 #endif
-    // shared thresholds: [nq] k-th-value words, then (8 B aligned) [nq][2] half-list words
+    // shared thresholds: [nq] k-th-value words, then (16 B aligned) [nq][8] union-group words
     if (kOut == 3) {  // swapped top-k: [nq] k-th-value words
         cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)a.nq * sizeof(uint32_t), s);
         if (e != cudaSuccess) return e;
@@ -941,8 +1009,9 @@ cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, 
         cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)a.nq * 4 * sizeof(uint32_t), s);
         if (e != cudaSuccess) return e;
     } else if (kOut == 0 && !(xmode & 16)) {  // diagnostic 16: keep caller-prefilled shared thresholds
-        const int64_t hoff = (a.nq + 1) & ~int64_t(1);
-        cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)(hoff + 2 * a.nq) * sizeof(uint32_t), s);
+        const int64_t hoff = (a.nq + 3) & ~int64_t(3);
+        const int64_t tq_count = ceil_div(a.nq, (kPairT ? 2 : 1) * C::QR);
+        cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)(hoff + 8 * a.nq + rparts * tq_count) * sizeof(uint32_t), s);
         if (e != cudaSuccess) return e;
     }
     return cudaLaunchKernelEx(&cfg, kern, a, k, index_base, vpp, tiles_q, part_keys, gthr, xmode, fo, omap);
