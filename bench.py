@@ -134,6 +134,16 @@ def measured_peaks():
             "sm_max_mhz": 1965.0}, "fallback"
 
 
+def int8_peak():
+    """Measured dense kind::i8 tensor rate (TOP/s at the max SM clock) from the
+    issue-rate probe (profiles/r2/int8_peak.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r2", "int8_peak.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f)
+    return None
+
+
 def profile_traffic(variant: str):
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(path):
@@ -521,11 +531,19 @@ def roofline(variant, n, m, nq, scan_ms, peaks, peak_src, clocks):
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     if variant == "tc":
         ops = 2.0 * 16 * m * dists
-        peak = 2.0 * peaks["bf16_tflops"] * 1e12
         achieved = ops / t
+        bf16x2 = 2.0 * peaks["bf16_tflops"] * 1e12
+        probe = int8_peak()
+        if probe:  # the measured kind::i8 issue rate (report against it)
+            peak = probe["int8_dense_tops"] * 1e12
+            src = (f"measured tcgen05 kind::i8 issue rate, {probe['dense_cycles_per_instr_k32']} cycles per "
+                   f"256x256x32 pair instruction at {probe['sm_mhz']} MHz (profiles/r2/int8_peak.json)")
+        else:
+            peak, src = bf16x2, f"int8 dense = 2 x {peak_src} bf16 ({peaks['bf16_tflops']} TFLOP/s)"
         return {"bound": "tensor", "achieved": round(achieved / 1e12, 2), "peak": round(peak / 1e12, 2),
                 "unit": "TOP/s", "frac": round(achieved / peak, 4), "traffic": profile_traffic("tc"),
-                "peak_source": f"int8 dense = 2 x {peak_src} bf16 ({peaks['bf16_tflops']} TFLOP/s)",
+                "peak_source": src,
+                "frac_vs_2x_bf16": round(achieved / bf16x2, 4),  # context: 2 x the driver's measured bf16 peak
                 "nominal_int8_frac": round(achieved / 4.5e15, 4),  # context: B200 dense int8 4.5 POP/s
                 "kernel": "bolt_topk (tcgen05 scan + top-k)", "kernel_ms": round(scan_ms, 4)}
     ops = 2.0 * m * dists
