@@ -64,8 +64,7 @@ namespace sp {
 
 using namespace tc;
 
-constexpr int kNQ = 224;                 // queries per MMA tile (N)
-constexpr int kNQH = kNQ / 2;            // query rows of B per CTA
+constexpr int kNQ = 224;                 // queries per MMA tile (N) of the large-batch instantiation
 constexpr int kVT = 256;                 // vectors per MMA tile (M, 128 per CTA)
 constexpr int kProdWarps = 4;           // thread = vector
 constexpr int kProducers = kProdWarps * 32;
@@ -73,29 +72,32 @@ constexpr int kEpiWarps = 8;
 constexpr int kEpilogue = kEpiWarps * 32;
 constexpr int kMmaWarp = kEpiWarps + kProdWarps;  // MMA issuer (leader CTA, one thread)
 constexpr int kThreads = (kMmaWarp + 1) * 32;
-constexpr int kQW = kNQ / 2;             // queries per epilogue warp
-constexpr int kNR = kQW / 2;             // packed registers per epilogue thread
-constexpr int kMetaCol0 = 2 * kNQ;       // TMEM: accumulators [0, 448), metadata [448, 512)
 constexpr int kRefresh = 4;              // tiles between reads of the shared thresholds
 constexpr uint32_t kNone = 0x7FFFu;      // "no threshold": every kv' <= 255 * 64 < 0x7FFF
 constexpr int kGroupRegs = 8;            // slow-path granularity: 8 registers = 16 queries
-constexpr int kNG = kNR / kGroupRegs;    // 7 groups per epilogue warp
 constexpr int kScrStride = 9;            // words per thread of the slow-path scratch (odd: conflict-free)
 
-template <int M, int KMAX>
+template <int M, int KMAX, int NQ_ = kNQ>
 struct Cfg {
+    static constexpr int NQ = NQ_;                  // queries per tile (N): 224, or 64 / 32 for small batches
+    static constexpr int NQH = NQ / 2;              // query rows of B per CTA
+    static constexpr int QW = NQ / 2;               // queries per epilogue warp (column half)
+    static constexpr int NR = QW / 2;               // packed registers per epilogue thread
+    static constexpr int NG = NR / kGroupRegs;      // slow-path groups of 16 queries per warp
+    static constexpr int META0 = 2 * NQ;            // TMEM: accumulators [0, 2 NQ), metadata ring after
+    static_assert(QW % 16 == 0 && NR % kGroupRegs == 0, "whole 16-query groups per warp");
     static constexpr int K = 16 * M;                // logical K bytes per row
     static constexpr int KC = 8 * M;                // compressed A bytes per vector
-    static constexpr int B_BYTES = kNQH * K;        // tables of this CTA's queries
+    static constexpr int B_BYTES = NQH * K;        // tables of this CTA's queries
     static constexpr int A_BYTES = 128 * KC;        // one stage: compressed one-hot of 128 vectors
     static constexpr int META_COLS = M / 2;         // TMEM metadata columns per stage
-    static constexpr int LIST_BYTES = kEpiWarps * kQW * KMAX * 4;
-    static constexpr int TQ_BYTES = kEpiWarps * kQW * 4;   // per-warp query thresholds (kv')
-    static constexpr int NT_BYTES = kEpiWarps * kNR * 4;   // per-warp packed filter words
+    static constexpr int LIST_BYTES = kEpiWarps * QW * KMAX * 4;
+    static constexpr int TQ_BYTES = kEpiWarps * QW * 4;   // per-warp query thresholds (kv')
+    static constexpr int NT_BYTES = kEpiWarps * NR * 4;   // per-warp packed filter words
     static constexpr int SCR_BYTES = kEpilogue * kScrStride * 4;  // slow path: one group's sums per thread
     static constexpr int FIXED = B_BYTES + LIST_BYTES + TQ_BYTES + NT_BYTES + SCR_BYTES + 256;
     static constexpr int S_SMEM = (227 * 1024 - FIXED) / A_BYTES;
-    static constexpr int S_TMEM = (512 - kMetaCol0) / META_COLS;
+    static constexpr int S_TMEM = (512 - META0) / META_COLS;
     static constexpr int S0 = S_SMEM < S_TMEM ? S_SMEM : S_TMEM;
     static constexpr int STAGES = S0 > 8 ? 8 : S0;
     static_assert(STAGES >= 2, "no room for a double-buffered stage");
@@ -112,7 +114,7 @@ struct Cfg {
     static constexpr int BAR_OFF = SCR_OFF + SCR_BYTES;
     static constexpr int SMEM = BAR_OFF + 256;
     // instruction descriptor: D s32, A/B u8, K-major, N = 224, M = 256, sparse (bit 2)
-    static constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(kNQ >> 3) << 17) | ((uint32_t)(256 >> 4) << 24) | 4u;
+    static constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(NQ >> 3) << 17) | ((uint32_t)(256 >> 4) << 24) | 4u;
 };
 
 __device__ __forceinline__ void mma_sp_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t meta, uint32_t idesc,
@@ -231,15 +233,16 @@ __device__ __noinline__ void slow_group(const uint32_t* __restrict__ scr, int g,
     }
 }
 
-template <int M, bool kDot, int KMAX>
+template <int M, bool kDot, int KMAX, int NQ>
 __global__ void __launch_bounds__(kThreads, 1)
 topk_sp_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, uint64_t* __restrict__ part_keys,
                uint32_t* __restrict__ gthr_inv, int xmode) {
 #ifndef BOLT_XMODE
     xmode = 0;  // diagnostic stage switches exist only in libbolt_x.so (tools/)
 #endif
-    using C = Cfg<M, KMAX>;
+    using C = Cfg<M, KMAX, NQ>;
     constexpr int S = C::STAGES;
+    constexpr int kNQH = C::NQH, kQW = C::QW, kNR = C::NR, kNG = C::NG, kMetaCol0 = C::META0;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sB = smem;
     uint8_t* sA = smem + C::A_OFF;
@@ -260,7 +263,7 @@ topk_sp_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
     const int unit = (int)(blockIdx.x >> 1);
     const int tq = unit % tiles_q;
     const int part = unit / tiles_q;
-    const int64_t qt0 = (int64_t)tq * kNQ;            // first query of the tile
+    const int64_t qt0 = (int64_t)tq * NQ;            // first query of the tile
     const int64_t q0 = qt0 + rank * kNQH;             // this CTA's B rows
     const int64_t vbeg = (int64_t)part * vpp;
     const int64_t vend = min64(a.n, vbeg + vpp);
@@ -430,18 +433,20 @@ topk_sp_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             tc_fence_after();
             uint32_t p[kNR];
             {
-                const uint32_t ta = tmem + tlane + (uint32_t)(d * kNQ + half * kQW);
+                const uint32_t ta = tmem + tlane + (uint32_t)(d * NQ + half * kQW);
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
+                for (int c = 0; c < kQW / 32; ++c) {
                     uint32_t r[16];
                     tmem_ld16p(ta + c * 32, r);
 #pragma unroll
                     for (int i = 0; i < 16; ++i) p[c * 16 + i] = r[i];
                 }
-                uint32_t r8[8];
-                tmem_ld8p(ta + 96, r8);
+                if constexpr (kQW % 32 == 16) {
+                    uint32_t r8[8];
+                    tmem_ld8p(ta + (kQW / 32) * 32, r8);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) p[48 + i] = r8[i];
+                    for (int i = 0; i < 8; ++i) p[(kQW / 32) * 16 + i] = r8[i];
+                }
                 tmem_wait_ld();
             }
             tc_fence_before();
@@ -521,7 +526,7 @@ topk_sp_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                     // A: compressed chunks 2 ks, 2 ks + 1 of the stage; B: table chunks 4 ks .. 4 ks + 3
                     const uint64_t ad = smem_desc(a_base + s * C::A_BYTES + 2 * ks * (128 * 16), 128 * 16, 128);
                     const uint64_t bd = smem_desc(b_base + 4 * ks * (kNQH * 16), kNQH * 16, 128);
-                    mma_sp_pair(tmem + (uint32_t)(d * kNQ), ad, bd,
+                    mma_sp_pair(tmem + (uint32_t)(d * NQ), ad, bd,
                                 tmem + (uint32_t)(kMetaCol0 + s * C::META_COLS + 2 * ks), C::IDESC, ks > 0 ? 1u : 0u);
                 }
                 mma_commit_pair(&empty[s]);
@@ -538,13 +543,13 @@ topk_sp_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
     }
 }
 
-template <int M, bool kDot, int KMAX>
+template <int M, bool kDot, int KMAX, int NQ>
 cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, uint64_t* part_keys, uint32_t* gthr,
                       cudaStream_t s) {
-    using C = Cfg<M, KMAX>;
-    const int tiles_q = (int)ceil_div(a.nq, kNQ);
+    using C = Cfg<M, KMAX, NQ>;
+    const int tiles_q = (int)ceil_div(a.nq, NQ);
     const int64_t vpp = ceil_div(ceil_div(a.n, rparts), 8) * 8;
-    auto kern = topk_sp_kernel<M, kDot, KMAX>;
+    auto kern = topk_sp_kernel<M, kDot, KMAX, NQ>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(2 * tiles_q * rparts));
@@ -567,20 +572,33 @@ cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, 
     return cudaLaunchKernelEx(&cfg, kern, a, k, index_base, vpp, tiles_q, part_keys, gthr, xmode);
 }
 
+template <int M, int NQ>
+cudaError_t launch_mq(const ScanArgs& a, int k, int metric, int64_t index_base, int rparts, uint64_t* part_keys,
+                      uint32_t* gthr, cudaStream_t s) {
+    const bool dot = metric == BOLT_DOT;
+    if (k <= 4 && NQ == kNQ)
+        return dot ? launch_mk<M, true, 4, NQ>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 4, NQ>(a, k, index_base, rparts, part_keys, gthr, s);
+    if (k <= 16 || M > 16)
+        return dot ? launch_mk<M, true, 16, NQ>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 16, NQ>(a, k, index_base, rparts, part_keys, gthr, s);
+    if constexpr (M <= 16)
+        return dot ? launch_mk<M, true, 32, NQ>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 32, NQ>(a, k, index_base, rparts, part_keys, gthr, s);
+    return cudaErrorInvalidValue;
+}
+
+// queries per tile: 32 or 64 for small batches (N = the batch, padded), else 224
+inline int pick_nq(int64_t nq) { return nq <= 32 ? 32 : (nq <= 64 ? 64 : kNQ); }
+
 template <int M>
 cudaError_t launch_m(const ScanArgs& a, int k, int metric, int64_t index_base, int rparts, uint64_t* part_keys,
                      uint32_t* gthr, cudaStream_t s) {
-    const bool dot = metric == BOLT_DOT;
-    if (k <= 4)
-        return dot ? launch_mk<M, true, 4>(a, k, index_base, rparts, part_keys, gthr, s)
-                   : launch_mk<M, false, 4>(a, k, index_base, rparts, part_keys, gthr, s);
-    if (k <= 16 || M > 16)
-        return dot ? launch_mk<M, true, 16>(a, k, index_base, rparts, part_keys, gthr, s)
-                   : launch_mk<M, false, 16>(a, k, index_base, rparts, part_keys, gthr, s);
-    if constexpr (M <= 16)
-        return dot ? launch_mk<M, true, 32>(a, k, index_base, rparts, part_keys, gthr, s)
-                   : launch_mk<M, false, 32>(a, k, index_base, rparts, part_keys, gthr, s);
-    return cudaErrorInvalidValue;
+    switch (pick_nq(a.nq)) {
+        case 32: return launch_mq<M, 32>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+        case 64: return launch_mq<M, 64>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+        default: return launch_mq<M, kNQ>(a, k, metric, index_base, rparts, part_keys, gthr, s);
+    }
 }
 
 }  // namespace sp
@@ -594,7 +612,7 @@ int topk_sp_supported(int64_t n, int m, int64_t nq, int k) {
 // fill >= 4 waves of SM pairs, each within the local index range
 int topk_sp_parts(int64_t n, int m, int64_t nq, int k, int num_sms) {
     (void)k;
-    const int64_t tiles_q = ceil_div(nq, sp::kNQ);
+    const int64_t tiles_q = ceil_div(nq, sp::pick_nq(nq));
     const int64_t max_range = m == 8 ? sp::Cfg<8, 4>::MAX_RANGE : (m == 16 ? sp::Cfg<16, 4>::MAX_RANGE
                                                                           : sp::Cfg<32, 4>::MAX_RANGE);
     int rparts = choose_parts(tiles_q, ceil_div(n, 8), num_sms / 2, (int64_t)256 * 16 / 8);
