@@ -46,8 +46,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c2")
     p.add_argument("--variant", default="auto", choices=["auto", "prmt", "tc"])
-    p.add_argument("--n", type=int, default=0, help="override rows per GPU (debug)")
-    p.add_argument("--nq", type=int, default=0, help="override queries (debug)")
+    p.add_argument("--n", "--rows", dest="n", type=int, default=0, help="override rows per GPU (debug)")
+    p.add_argument("--nq", "--queries", dest="nq", type=int, default=0, help="override queries (debug)")
     p.add_argument("--k", type=int, default=0, help="override top-k (debug, c5)")
     p.add_argument("--parallel", default="row", choices=["row", "query"],
                    help="c5 with N > 1: row-sharded database (all-gather + merge) or replicated database with "
@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--e2e-chunks", type=int, default=8, help="row blocks of the copy/compute-overlapped host search")
     p.add_argument("--no-graph", action="store_true", help="time the step eagerly instead of a CUDA graph")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="gloo: CPU collectives, for testing the N > 1 glue with several ranks on one GPU "
+                        "(never a measurement)")
     return p.parse_args()
 
 
@@ -259,10 +262,14 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    local = local % torch.cuda.device_count()  # --dist-backend gloo: several ranks may share one GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg, n, nq = workload(args, rank)
     metric = cfg.metrics[0]
     k = cfg.k
@@ -374,12 +381,17 @@ def run_ours(args):
     scan_ms = sum(a.elapsed_time(b) for a, b in ev_scan) / len(ev_scan)
     ms = ms_local
     if world > 1:
-        t = torch.tensor([ms_local, scan_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_local, scan_ms], dtype=torch.float64, device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, scan_ms = float(t[0]), float(t[1])
     ms_step = ms / args.steps
     dists = world * n * nq
     value = dists / (ms_step * 1e-3) / 1e9
+
+    exact = None
+    if world > 1 and not full:  # the timed step's merged keys against one GPU's scan of all rows
+        exact = check_sharded(bolt, codes, n, cfg.m, ql, final, k, metric, variant, dev)
+        final_timed = final.clone()
 
     # --- e2e through the public host-buffer API (H2D of X, Q inside the timed region)
     e2e = None
@@ -418,7 +430,7 @@ def run_ours(args):
         kd = torch.empty((nq, k), dtype=torch.uint64, device=dev)
 
         def e2e_step():
-            hs(Xh, Qh, model.C, metric, model.a, model.b, kh)
+            hs(Xh, Qh, model.C, metric, model.a, model.b, kh, index_base=rank * n)
             if world > 1:
                 kd.copy_(kh, non_blocking=True)
                 bolt.topk_merge(gather_keys(kd), out=final)
@@ -436,18 +448,19 @@ def run_ours(args):
         torch.cuda.synchronize()
         e_ms = a0.elapsed_time(a1) / args.e2e_steps
         if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev if args.dist_backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t[0])
+        if world > 1:  # the host-buffer path (global row indices via index_base) returns the same keys
+            if not torch.equal(final.view(torch.int64), final_timed.view(torch.int64)):
+                raise SystemExit("e2e (host-buffer) sharded keys differ from the device path's")
+            exact["e2e_keys_equal"] = True
         e2e = {"value": round(dists / (e_ms * 1e-3) / 1e9, 4), "unit": UNIT,
                "h2d_bytes_per_step": int(X.nbytes + Q.nbytes),
                "d2h_bytes_per_step": int(nq * k * 8), "ms_per_step": round(e_ms, 3),
                "api": f"bolt_search_host{'_pipelined' if args.e2e_chunks > 1 else ''} (pinned host X, Q -> keys"
                       f"{f'; X in {args.e2e_chunks} blocks overlapped with encode + scan' if args.e2e_chunks > 1 else ''})"}
 
-    exact = None
-    if world > 1 and not full:
-        exact = check_sharded(bolt, codes, n, cfg.m, ql, final, k, metric, variant, dev)
 
     # --- roofline of the dominant kernel (scan + fused top-k, or the full-output scan)
     peaks, peak_src = measured_peaks()
@@ -628,10 +641,14 @@ def run_c5(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    local = local % torch.cuda.device_count()  # --dist-backend gloo: several ranks may share one GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = G.CONFIGS["c5"]
     n_total = args.n or cfg.n
     nq, k, metric, m = args.nq or cfg.nq, args.k or cfg.k, cfg.metrics[0], cfg.m
@@ -697,7 +714,7 @@ def run_c5(args):
     ms = t_start.elapsed_time(t_end)
     scan_ms = sum(a.elapsed_time(b) for a, b in ev) / len(ev)
     if world > 1:
-        t = torch.tensor([ms, scan_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, scan_ms], dtype=torch.float64, device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, scan_ms = float(t[0]), float(t[1])
     ms_step = ms / args.steps
@@ -724,7 +741,7 @@ def run_c5(args):
         torch.cuda.synchronize()
         e_ms = a0.elapsed_time(a1) / args.e2e_steps
         if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev if args.dist_backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t[0])
         e2e = {"value": round(n_total * nq / (e_ms * 1e-3) / 1e9, 4), "unit": UNIT,

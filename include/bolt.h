@@ -257,6 +257,12 @@ BOLT_API bolt_status bolt_search_host(const float* X_host, int64_t n, int j, con
                              int64_t nq, const float* C, int m, bolt_metric metric, float a,
                              const float* b, int k, uint64_t* keys_host, void* ws,
                              size_t ws_bytes, bolt_stream_t stream);
+/* As bolt_search_host with the rows' global index base (a row shard
+ * starting at row index_base of a larger database; index_base + n < 2^48). */
+BOLT_API bolt_status bolt_search_host_ex(const float* X_host, int64_t n, int j, const float* Q_host,
+                                         int64_t nq, const float* C, int m, bolt_metric metric, float a,
+                                         const float* b, int k, int64_t index_base, uint64_t* keys_host, void* ws,
+                                         size_t ws_bytes, bolt_stream_t stream);
 
 /* Same search with the host->device copy of X overlapped with the compute:
  * X crosses in `chunks` row blocks (boundaries at multiples of 256 rows) on
@@ -271,6 +277,12 @@ BOLT_API bolt_status bolt_search_host_pipelined(const float* X_host, int64_t n, 
                                                 const float* b, int k, uint64_t* keys_host, void* ws,
                                                 size_t ws_bytes, int chunks, bolt_stream_t stream,
                                                 bolt_stream_t copy_stream);
+/* As bolt_search_host_pipelined with the rows' global index base. */
+BOLT_API bolt_status bolt_search_host_pipelined_ex(const float* X_host, int64_t n, int j, const float* Q_host,
+                                                   int64_t nq, const float* C, int m, bolt_metric metric, float a,
+                                                   const float* b, int k, int64_t index_base, uint64_t* keys_host,
+                                                   void* ws, size_t ws_bytes, int chunks, bolt_stream_t stream,
+                                                   bolt_stream_t copy_stream);
 
 /* ----------------------------------------------- offline fit */
 /* k-means codebooks (R8): per subspace, centroids start at rows

@@ -307,7 +307,9 @@ class HostSearch:
         self.workspace = torch.empty(wsb, dtype=torch.uint8, device=self.device)
 
     def __call__(self, X_host: torch.Tensor, Q_host: torch.Tensor, C: torch.Tensor, metric, a: float,
-                 b: torch.Tensor, keys_host: torch.Tensor) -> torch.Tensor:
+                 b: torch.Tensor, keys_host: torch.Tensor, index_base: int = 0) -> torch.Tensor:
+        """keys_host [nq][k] u64 <- top-k of the rows of X_host, whose global
+        indices start at index_base (a row shard of a larger database)."""
         for t, nm in ((X_host, "X_host"), (Q_host, "Q_host")):
             if t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
                 raise TypeError(f"{nm} must be a contiguous fp32 host tensor")
@@ -316,13 +318,13 @@ class HostSearch:
         _cuda(C, "C", torch.float32)
         _cuda(b, "b", torch.float32)
         if self.chunks > 1:
-            _lib.call("bolt_search_host_pipelined", X_host.data_ptr(), self.n, self.j, Q_host.data_ptr(), self.nq,
-                      C.data_ptr(), self.m, _metric(metric), float(a), b.data_ptr(), self.k,
+            _lib.call("bolt_search_host_pipelined_ex", X_host.data_ptr(), self.n, self.j, Q_host.data_ptr(), self.nq,
+                      C.data_ptr(), self.m, _metric(metric), float(a), b.data_ptr(), self.k, int(index_base),
                       keys_host.data_ptr(), self.workspace.data_ptr(), self.workspace.numel(), self.chunks,
                       _stream(self.device), self.copy_stream.cuda_stream)
         else:
-            _lib.call("bolt_search_host", X_host.data_ptr(), self.n, self.j, Q_host.data_ptr(), self.nq,
-                      C.data_ptr(), self.m, _metric(metric), float(a), b.data_ptr(), self.k,
+            _lib.call("bolt_search_host_ex", X_host.data_ptr(), self.n, self.j, Q_host.data_ptr(), self.nq,
+                      C.data_ptr(), self.m, _metric(metric), float(a), b.data_ptr(), self.k, int(index_base),
                       keys_host.data_ptr(), self.workspace.data_ptr(), self.workspace.numel(),
                       _stream(self.device))
         return keys_host

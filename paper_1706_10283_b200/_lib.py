@@ -49,6 +49,9 @@ SIGNATURES = {
     "bolt_keys_split_f32": ([_P, _I64, _I32, _P, _P, _P], _I32),
     "bolt_search_host_workspace_bytes": ([_I64, _I32, _I32, _I64, _I32], _SZ),
     "bolt_search_host": ([_P, _I64, _I32, _P, _I64, _P, _I32, _I32, _F32, _P, _I32, _P, _P, _SZ, _P], _I32),
+    "bolt_search_host_ex": ([_P, _I64, _I32, _P, _I64, _P, _I32, _I32, _F32, _P, _I32, _I64, _P, _P, _SZ, _P], _I32),
+    "bolt_search_host_pipelined_ex": ([_P, _I64, _I32, _P, _I64, _P, _I32, _I32, _F32, _P, _I32, _I64, _P, _P, _SZ,
+                                       _I32, _P, _P], _I32),
     "bolt_search_host_pipelined_workspace_bytes": ([_I64, _I32, _I32, _I64, _I32, _I32], _SZ),
     "bolt_search_host_pipelined": ([_P, _I64, _I32, _P, _I64, _P, _I32, _I32, _F32, _P, _I32, _P, _P, _SZ, _I32,
                                     _P, _P], _I32),

@@ -587,6 +587,13 @@ bolt_status bolt_search_host(const float* X_host, int64_t n, int j, const float*
                              int64_t nq, const float* C, int m, bolt_metric metric, float a,
                              const float* b, int k, uint64_t* keys_host, void* ws,
                              size_t ws_bytes, bolt_stream_t stream) {
+    return bolt_search_host_ex(X_host, n, j, Q_host, nq, C, m, metric, a, b, k, 0, keys_host, ws, ws_bytes, stream);
+}
+
+bolt_status bolt_search_host_ex(const float* X_host, int64_t n, int j, const float* Q_host,
+                                int64_t nq, const float* C, int m, bolt_metric metric, float a,
+                                const float* b, int k, int64_t index_base, uint64_t* keys_host, void* ws,
+                                size_t ws_bytes, bolt_stream_t stream) {
     TRY(check_jm(j, m));
     if (n < 1 || nq < 0) return fail(BOLT_E_SHAPE, "n must be >= 1, nq >= 0");
     if (k < 1 || k > kMaxK) return fail(BOLT_E_SHAPE, "k = %d outside 1..128", k);
@@ -611,7 +618,7 @@ bolt_status bolt_search_host(const float* X_host, int64_t n, int j, const float*
     TRY(cuda_status(cudaMemcpyAsync(Qd, Q_host, (size_t)nq * j * sizeof(float), cudaMemcpyHostToDevice, s), "H2D Q"));
     TRY(bolt_encode(Xd, n, j, j, C, m, codes, stream));
     TRY(bolt_build_quantized_luts(Qd, nq, j, j, C, m, metric, a, b, ql, nullptr, stream));
-    TRY(bolt_topk(codes, n, m, ql, nq, k, metric, 0, keys, tws, tws_bytes, stream));
+    TRY(bolt_topk(codes, n, m, ql, nq, k, metric, index_base, keys, tws, tws_bytes, stream));
     return cuda_status(cudaMemcpyAsync(keys_host, keys, (size_t)nq * k * sizeof(uint64_t), cudaMemcpyDeviceToHost, s), "D2H keys");
 }
 
@@ -648,6 +655,14 @@ bolt_status bolt_search_host_pipelined(const float* X_host, int64_t n, int j, co
                                        const float* C, int m, bolt_metric metric, float a, const float* b, int k,
                                        uint64_t* keys_host, void* ws, size_t ws_bytes, int chunks,
                                        bolt_stream_t stream, bolt_stream_t copy_stream) {
+    return bolt_search_host_pipelined_ex(X_host, n, j, Q_host, nq, C, m, metric, a, b, k, 0, keys_host, ws, ws_bytes,
+                                         chunks, stream, copy_stream);
+}
+
+bolt_status bolt_search_host_pipelined_ex(const float* X_host, int64_t n, int j, const float* Q_host, int64_t nq,
+                                          const float* C, int m, bolt_metric metric, float a, const float* b, int k,
+                                          int64_t index_base, uint64_t* keys_host, void* ws, size_t ws_bytes,
+                                          int chunks, bolt_stream_t stream, bolt_stream_t copy_stream) {
     TRY(check_jm(j, m));
     if (n < 1 || nq < 0) return fail(BOLT_E_SHAPE, "n must be >= 1, nq >= 0");
     if (k < 1 || k > kMaxK) return fail(BOLT_E_SHAPE, "k = %d outside 1..128", k);
@@ -702,7 +717,7 @@ bolt_status bolt_search_host_pipelined(const float* X_host, int64_t n, int j, co
         cudaEventDestroy(ev[i]);
         uint32_t* cw = codes + (r0 / 8) * m;
         TRY(bolt_encode(Xd + r0 * j, r1 - r0, j, j, C, m, cw, stream));
-        TRY(bolt_topk(cw, r1 - r0, m, ql, nq, k, metric, r0, used == 1 ? keys : parts + (size_t)i * nq * k, tws,
+        TRY(bolt_topk(cw, r1 - r0, m, ql, nq, k, metric, index_base + r0, used == 1 ? keys : parts + (size_t)i * nq * k, tws,
                       tws_bytes, stream));
     }
     if (used > 1) TRY(bolt_topk_merge(parts, used, nq, k, keys, stream));

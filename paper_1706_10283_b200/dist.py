@@ -25,13 +25,25 @@ def shard_range(n_total: int, world: int, rank: int) -> tuple[int, int]:
     return r0, r1
 
 
+def _all_gather_into(out: torch.Tensor, src: torch.Tensor, group=None) -> None:
+    """all_gather_into_tensor; under gloo (CPU collectives: the multi-process
+    glue tests, and bench.py --dist-backend gloo with several ranks on one
+    GPU) device tensors travel through host copies."""
+    if dist.get_backend(group) == "gloo" and src.is_cuda:
+        host = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(host, src.cpu(), group=group)
+        out.copy_(host)
+    else:
+        dist.all_gather_into_tensor(out, src, group=group)
+
+
 def gather_keys(keys: torch.Tensor, group=None) -> torch.Tensor:
     """[nq][k] u64 keys of every rank -> [W][nq][k] (all_gather_into_tensor).
     The collective moves the bits as int64 (backends lack unsigned 64-bit)."""
     world = dist.get_world_size(group)
     src = keys.contiguous().view(torch.int64)
     out = torch.empty((world * keys.shape[0],) + tuple(keys.shape[1:]), dtype=torch.int64, device=keys.device)
-    dist.all_gather_into_tensor(out, src, group=group)
+    _all_gather_into(out, src, group)
     return out.view(torch.uint64).view((world,) + tuple(keys.shape))
 
 
@@ -42,7 +54,8 @@ def gather_codes(codes: torch.Tensor, n_local: int, m: int, group=None) -> tuple
     rank may end in a partial group.  Used to check a sharded result against
     one device's scan of all rows (bench.py --gpus N)."""
     world, rank = dist.get_world_size(group), dist.get_rank(group)
-    mine = torch.tensor([n_local], dtype=torch.int64, device=codes.device)
+    mine = torch.tensor([n_local], dtype=torch.int64,
+                        device="cpu" if dist.get_backend(group) == "gloo" else codes.device)
     ns = [torch.zeros_like(mine) for _ in range(world)]
     dist.all_gather(ns, mine, group=group)
     ns = [int(x.item()) for x in ns]
@@ -53,7 +66,7 @@ def gather_codes(codes: torch.Tensor, n_local: int, m: int, group=None) -> tuple
     pad = torch.zeros(wmax, dtype=torch.int32, device=codes.device)
     pad[:words[rank]] = codes[:words[rank]].view(torch.int32)
     out = torch.empty(world * wmax, dtype=torch.int32, device=codes.device)
-    dist.all_gather_into_tensor(out, pad, group=group)
+    _all_gather_into(out, pad, group)
     whole = torch.cat([out[r * wmax:r * wmax + words[r]] for r in range(world)])
     return whole.view(torch.uint32), sum(ns)
 
@@ -86,7 +99,7 @@ def gather_query_slices(local: torch.Tensor, nq: int, group=None) -> torch.Tenso
     pad = torch.full((per, k), -1, dtype=torch.int64, device=local.device)
     pad[:local.shape[0]] = local.contiguous().view(torch.int64)
     out = torch.empty((world * per, k), dtype=torch.int64, device=local.device)
-    dist.all_gather_into_tensor(out, pad, group=group)
+    _all_gather_into(out, pad, group)
     return out[:nq].view(torch.uint64)
 
 

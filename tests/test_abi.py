@@ -77,7 +77,9 @@ def test_workspace_sizing_host(lib):
     # the plan is a pure function of the shapes (and SM count): partial lists
     # [parts][nq][k] u64, then the shared per-query threshold words: one
     # (PRMT), 33 (small-batch PRMT kernel, nq < 64 and m in {8,16,32}: k-th
-    # value + 32 minima slots), 3 nq + 1 (tcgen05: k-th value + half-list pairs)
+    # value + 32 minima slots), 9 nq + 4 + rparts ceil(nq / 128) (tcgen05: k-th
+    # value words, 16 B aligned rows of 8 union-group words, finished-partition
+    # counters)
     for n, m, nq, k, variant in [(10, 8, 4, 10, 1), (1_000_000, 16, 10_000, 10, 1), (10**8, 16, 1, 100, 1),
                                  (5000, 12, 8, 10, 1), (1_000_000, 16, 10_000, 10, 2), (777, 32, 300, 32, 2)]:
         ws = lib.bolt_topk_workspace_bytes_ex(n, m, nq, k, variant)
@@ -86,7 +88,7 @@ def test_workspace_sizing_host(lib):
         assert rv.value == variant
         p = parts.value
         if variant == 2:
-            expect = p * nq * k * 8 + (3 * nq + 1) * 4
+            expect = p * nq * k * 8 + (9 * nq + 4 + (p // 2) * -(-nq // 128)) * 4
         elif nq < 64 and m in (8, 16, 32):
             expect = p * nq * k * 8 + 33 * nq * 4
         else:
