@@ -178,7 +178,7 @@ bolt_status bolt_encode_ex(const float* X, int64_t n, int j, int64_t ldx, const 
     DevInfo d;
     TRY(device_info(&d));
     return cuda_status(launch_encode(X, n, j, ldx, C, m, codes, d.sms, (cudaStream_t)stream,
-                                     variant != BOLT_ENCODE_EXPANDED),
+                                     variant == BOLT_ENCODE_DIRECT ? 1 : variant == BOLT_ENCODE_EXPANDED ? 2 : 0),
                        "bolt_encode");
 }
 

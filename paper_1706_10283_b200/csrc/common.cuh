@@ -97,10 +97,11 @@ struct ScanArgs {
 // return cudaGetLastError() of their launch.
 namespace bolt {
 // sms: the device's SM count (block-size heuristic), passed down from the ABI's device cache
-// direct: the direct-difference kernels only (else the fast expanded-distance
-// kernel for J/M = 8 / 16, bit-identical by its bound + fallback)
+// mode: 0 auto / 1 direct: the direct-difference kernels; 2 (J/M = 8): the
+// TMA-staged expanded-distance kernel, the same codes by its bound + direct
+// fallback (measured no faster: DESIGN.md 6.3)
 cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,
-                          uint32_t* codes, int sms, cudaStream_t s, bool direct = false);
+                          uint32_t* codes, int sms, cudaStream_t s, int mode = 0);
 // Bolt No Quantize (scan_f32.cu): fp32 tables, fp32 sums, R18 keys
 int topk_f32_parts(int64_t n, int64_t nq, int num_sms);
 cudaError_t launch_scan_f32(const uint32_t* codes, int64_t n, int m, const float* luts, int64_t nq, float* out,

@@ -12,6 +12,8 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tc_ptx.cuh"
+#include "tma_host.cuh"
 
 namespace bolt {
 namespace {
@@ -270,7 +272,7 @@ __device__ __noinline__ uint32_t direct_argmin(const float* __restrict__ x, cons
     return arg;
 }
 
-// Fast path for L = 8 / 16 (same data flow as encode_l8_kernel): per
+// Expanded distances (BOLT_ENCODE_EXPANDED): per
 // centroid s_k = fl(||c_k||^2) + sum_t x_t (-2 c_kt) as one packed FFMA chain
 // (one FFMA per (dimension, centroid) instead of a subtract and an FFMA),
 // which orders the centroids like ||x - c_k||^2 up to a rigorous rounding
@@ -287,24 +289,53 @@ __device__ __noinline__ uint32_t direct_argmin(const float* __restrict__ x, cons
 // need = 2.5 E + 3 g(L+2)(X2 + |b1| + E) (X2 >= ||x||^2), the direct
 // distances keep the same unique minimum.  The factors carry a >= 25 % slack
 // for the rounding of the test itself.
-template <int L, int THREADS, int MINB = 2>
-__global__ void __launch_bounds__(THREADS, MINB * 256 / THREADS)
-encode_fast_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const float* __restrict__ C, int m,
-                   uint32_t* __restrict__ codes) {
-    extern __shared__ float4 enc_smem4[];
-    static_assert(L == 8 || L == 16, "32-byte row slices");
-    constexpr int NL = L / 8;
+//
+// The kernel stages the row slices of a codebook in shared memory by 2-D
+// tensor copies (one 256-row x 32-byte box per half block) instead of
+// register loads (a register-loading version of the same arithmetic ran at
+// 0.24 ms on c2, its loads exposed; ncu profiles/r2/ncu_full_enc_*.txt).
+// Warp 8 issues the copies kEncStages slices ahead; warps 0-7 (thread t =
+// local rows t and t + 256) rank the centroids and pack the layout-v1 words
+// with shuffles.  Measured c2: 0.205 ms against the direct kernel's 0.199 --
+// no faster, so it is the explicit variant, not the default.
+constexpr int kEncStages = 4;
+constexpr int kTmaRows = 512;               // rows per block
+constexpr int kTmaWorkers = 256;            // compute threads (2 rows each)
+
+template <int L>
+__global__ void __launch_bounds__(kTmaWorkers + 32, 2)
+encode_tma_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ X, int64_t n, int64_t ldx,
+                  const float* __restrict__ C, int m, uint32_t* __restrict__ codes) {
+    static_assert(L == 8, "32-byte row slices");
+    extern __shared__ __align__(1024) uint8_t enc_tma_smem[];
     constexpr float kU = 5.9604645e-8f;  // 2^-24
     constexpr float kGL = (float)L * kU / (1.0f - (float)L * kU);
     constexpr float kGL2 = (float)(L + 2) * kU / (1.0f - (float)(L + 2) * kU);
+    constexpr int SLICE = kTmaRows * L * 4;  // bytes of one codebook's row slices
     const int j = m * L;
-    float* cneg = reinterpret_cast<float*>(enc_smem4);           // [m][L][16] -c (direct fallback)
-    float* cm2 = cneg + (size_t)j * kK;                           // [m][L][16] -2c
-    float* cn = cm2 + (size_t)j * kK;                             // [m][16]    fl(||c_k||^2)
-    float* amax = cn + (size_t)m * kK;                            // [m][L]     max_k |c_kt|
-    float* c2max = amax + (size_t)j;                              // [m]        bound on max_k n_k
-    uint32_t* stage = reinterpret_cast<uint32_t*>(c2max + ((m + 3) & ~3));  // [GPB][m]
-    for (int e = threadIdx.x; e < j * kK; e += blockDim.x) {
+    float* xs = reinterpret_cast<float*>(enc_tma_smem);                 // [S][512][L]
+    float* cneg = xs + kEncStages * kTmaRows * L;                        // [m][L][16] -c
+    float* cm2 = cneg + (size_t)j * kK;                                  // [m][L][16] -2c
+    float* cn = cm2 + (size_t)j * kK;                                    // [m][16]
+    float* amax = cn + (size_t)m * kK;                                   // [m][L]
+    float* c2max = amax + (size_t)j;                                     // [m]
+    uint32_t* stage = reinterpret_cast<uint32_t*>(c2max + ((m + 3) & ~3));  // [64][m]
+    uint64_t* full = reinterpret_cast<uint64_t*>(stage + (size_t)(kTmaRows / kRowsPerWord) * m + 2);  // 8 B aligned
+    full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
+    uint64_t* empty = full + kEncStages;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t row_blk = (int64_t)blockIdx.x * kTmaRows;
+    if (tid == 0) {
+        for (int i = 0; i < kEncStages; ++i) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&empty[i], kTmaWorkers / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // centroid tables (all threads), before the copy warp enters its loop: a
+    // block barrier after that point would deadlock against its empty-slot waits
+    for (int e = tid; e < j * kK; e += blockDim.x) {
         int c = e / (kK * L);
         int r = e - c * kK * L;
         int k = r / L;
@@ -312,82 +343,75 @@ encode_fast_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const fl
         cneg[((size_t)c * L + d) * kK + k] = -C[e];
         cm2[((size_t)c * L + d) * kK + k] = -2.0f * C[e];
     }
-    for (int e = threadIdx.x; e < m * kK; e += blockDim.x) {
+    for (int e = tid; e < m * kK; e += blockDim.x) {
         const float* ck = C + (size_t)e * L;
         float acc = 0.f;
         for (int t = 0; t < L; ++t) acc = __fmaf_rn(ck[t], ck[t], acc);
         cn[e] = acc;
     }
-    for (int e = threadIdx.x; e < j; e += blockDim.x) {
+    for (int e = tid; e < j; e += blockDim.x) {
         const int c = e / L, t = e - c * L;
         float a = 0.f;
         for (int k = 0; k < kK; ++k) a = fmaxf(a, fabsf(C[((size_t)c * kK + k) * L + t]));
         amax[e] = a;
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < m; c += blockDim.x) {
+    for (int c = tid; c < m; c += blockDim.x) {
         float a = 0.f;
         for (int k = 0; k < kK; ++k) a = fmaxf(a, fabsf(cn[c * kK + k]));
         c2max[c] = a * (1.0f + 2.0f * kGL);
     }
     __syncthreads();
-    constexpr int RPB = THREADS * kEnc2Rows, GPB = RPB / kRowsPerWord;
-    const int64_t row0 = (int64_t)blockIdx.x * RPB + threadIdx.x * kEnc2Rows;
-    const float4* xr[kEnc2Rows];
-    bool valid[kEnc2Rows];
+    if (warp == kTmaWorkers / 32) {
+        // ------------------------------------------------ copy warp
+        if (lane == 0) {
+            for (int c = 0; c < m; ++c) {
+                const int s = c % kEncStages;
+                tc::mbar_wait(&empty[s], ((c / kEncStages) & 1) ^ 1);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(&full[s])),
+                             "r"(SLICE)
+                             : "memory");
 #pragma unroll
-    for (int r = 0; r < kEnc2Rows; ++r) {
-        valid[r] = row0 + r < n;
-        xr[r] = reinterpret_cast<const float4*>(X + (valid[r] ? (row0 + r) : 0) * ldx);
+                for (int h = 0; h < 2; ++h)
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+                            "r"(tc::smem_u32(xs + ((size_t)s * kTmaRows + h * 256) * L)),
+                        "l"(&xmap), "r"(c * L), "r"((int)(row_blk + h * 256)), "r"(tc::smem_u32(&full[s]))
+                        : "memory");
+            }
+        }
+        return;
     }
-    // row slices prefetched two codebooks ahead (a ring of two register
-    // buffers, indexed statically by unrolling the codebook loop by 2): the
-    // expanded distances leave too little compute per load to hide one slice
-    constexpr int PD = 2;
-    float4 nxr[PD][kEnc2Rows][2 * NL];
-    auto load_slice = [&](int c, float4 (&buf)[kEnc2Rows][2 * NL]) {
+    // ---------------------------------------------------- compute warps
+    uint64_t amb[2] = {0ull, 0ull};
+    const bool valid[2] = {row_blk + tid < n, row_blk + tid + 256 < n};
+    for (int c = 0; c < m; ++c) {
+        const int s = c % kEncStages;
+        tc::mbar_wait(&full[s], (c / kEncStages) & 1);
+        float xv[2][L];
 #pragma unroll
-        for (int r = 0; r < kEnc2Rows; ++r)
-#pragma unroll
-            for (int h = 0; h < NL; ++h) {
-                if (valid[r] && c < m)
-                    ldg256(reinterpret_cast<const float*>(xr[r] + 2 * NL * c + 2 * h), buf[r][2 * h], buf[r][2 * h + 1]);
-                else buf[r][2 * h] = buf[r][2 * h + 1] = make_float4(0, 0, 0, 0);
-            }
-    };
-#pragma unroll
-    for (int j = 0; j < PD; ++j) load_slice(j, nxr[j]);
-    uint64_t amb[kEnc2Rows] = {};  // codebooks (bit c) whose argmin the bound leaves ambiguous
-    for (int c0 = 0; c0 < m; c0 += PD)
-#pragma unroll
-    for (int jj = 0; jj < PD; ++jj) {
-        const int c = c0 + jj;
-        if (c >= m) break;
-        float xv[kEnc2Rows][L];
-#pragma unroll
-        for (int r = 0; r < kEnc2Rows; ++r)
-#pragma unroll
-            for (int h = 0; h < 2 * NL; ++h) {
-                xv[r][4 * h] = nxr[jj][r][h].x; xv[r][4 * h + 1] = nxr[jj][r][h].y;
-                xv[r][4 * h + 2] = nxr[jj][r][h].z; xv[r][4 * h + 3] = nxr[jj][r][h].w;
-            }
-        if (c + PD < m) load_slice(c + PD, nxr[jj]);
-        // s_k = n_k + sum_t x_t (-2 c_kt), packed over centroid pairs; (x^2, |x| amax) alongside
-        float2 sv[kEnc2Rows][kK / 2];
-        float2 xa[kEnc2Rows];
+        for (int r = 0; r < 2; ++r) {
+            const float4* xp = reinterpret_cast<const float4*>(xs + ((size_t)s * kTmaRows + tid + 256 * r) * L);
+            const float4 a0 = xp[0], a1 = xp[1];
+            xv[r][0] = a0.x; xv[r][1] = a0.y; xv[r][2] = a0.z; xv[r][3] = a0.w;
+            xv[r][4] = a1.x; xv[r][5] = a1.y; xv[r][6] = a1.z; xv[r][7] = a1.w;
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&empty[s]);  // the slice is in registers
+        float2 sv[2][kK / 2];
+        float2 xa[2];
         {
             const float4* cn4 = reinterpret_cast<const float4*>(cn + c * kK);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const float4 v = cn4[q];
 #pragma unroll
-                for (int r = 0; r < kEnc2Rows; ++r) {
+                for (int r = 0; r < 2; ++r) {
                     sv[r][2 * q] = make_float2(v.x, v.y);
                     sv[r][2 * q + 1] = make_float2(v.z, v.w);
                 }
             }
-#pragma unroll
-            for (int r = 0; r < kEnc2Rows; ++r) xa[r] = make_float2(0.f, 0.f);
+            xa[0] = xa[1] = make_float2(0.f, 0.f);
         }
         const float* cc = cm2 + (size_t)c * L * kK;
         const float* am = amax + c * L;
@@ -400,21 +424,19 @@ encode_fast_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const fl
                 float4 c4 = cv[q];
                 float2 ca = make_float2(c4.x, c4.y), cb = make_float2(c4.z, c4.w);
 #pragma unroll
-                for (int r = 0; r < kEnc2Rows; ++r) {
+                for (int r = 0; r < 2; ++r) {
                     float2 xx = make_float2(xv[r][t], xv[r][t]);
                     sv[r][2 * q] = __ffma2_rn(xx, ca, sv[r][2 * q]);
                     sv[r][2 * q + 1] = __ffma2_rn(xx, cb, sv[r][2 * q + 1]);
                 }
             }
 #pragma unroll
-            for (int r = 0; r < kEnc2Rows; ++r)
+            for (int r = 0; r < 2; ++r)
                 xa[r] = __ffma2_rn(make_float2(xv[r][t], fabsf(xv[r][t])), make_float2(xv[r][t], at), xa[r]);
         }
         const float c2 = c2max[c];
-        uint32_t quarter = 0;  // this thread's 2 rows (8 bits)
 #pragma unroll
-        for (int r = 0; r < kEnc2Rows; ++r) {
-            // minimum as a depth-4 tree (the chains, not the pipes, bound this phase)
+        for (int r = 0; r < 2; ++r) {
             float mn[kK / 2];
 #pragma unroll
             for (int p = 0; p < kK / 2; ++p) mn[p] = fminf(sv[r][p].x, sv[r][p].y);
@@ -426,7 +448,7 @@ encode_fast_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const fl
             const float E = 4.0f * kGL * (c2 + 2.0f * xa[r].y * (1.0f + 2.0f * kGL));
             const float need = 2.5f * E + 3.0f * kGL2 * (xa[r].x * (1.0f + 2.0f * kGL) + fabsf(b1) + E);
             const float thr = b1 + need;
-            uint32_t bl[kK / 2];  // centroids within the bound of the minimum, OR-reduced as a tree
+            uint32_t bl[kK / 2];
 #pragma unroll
             for (int p = 0; p < kK / 2; ++p)
                 bl[p] = ((sv[r][p].x < thr ? 1u : 0u) | (sv[r][p].y < thr ? 2u : 0u)) << (2 * p);
@@ -436,36 +458,36 @@ encode_fast_kernel(const float* __restrict__ X, int64_t n, int64_t ldx, const fl
                 for (int p = 0; p < w; ++p) bl[p] |= bl[p + w];
             const uint32_t below = bl[0];
             uint32_t arg = __ffs(below) - 1;
-            if (__popc(below) != 1) amb[r] |= 1ull << c;  // ambiguous: redone by direct differences below
+            if (__popc(below) != 1 && valid[r]) amb[r] |= 1ull << c;
             if (!valid[r]) arg = 0;
-            quarter |= arg << (4 * r);
+            // layout-v1 word of this row's group: 8 consecutive lanes hold its 8 rows
+            uint32_t v = (arg & 0xFu) << (4 * (tid & 7));
+            v |= __shfl_xor_sync(0xffffffffu, v, 1);
+            v |= __shfl_xor_sync(0xffffffffu, v, 2);
+            v |= __shfl_xor_sync(0xffffffffu, v, 4);
+            if ((tid & 7) == 0) stage[((tid + 256 * r) >> 3) * m + c] = v;
         }
-        const uint32_t q1 = __shfl_down_sync(0xffffffffu, quarter, 1);
-        const uint32_t q2 = __shfl_down_sync(0xffffffffu, quarter, 2);
-        const uint32_t q3 = __shfl_down_sync(0xffffffffu, quarter, 3);
-        if ((threadIdx.x & 3) == 0) stage[(threadIdx.x >> 2) * m + c] = quarter | (q1 << 8) | (q2 << 16) | (q3 << 24);
     }
-    // ambiguous (row, codebook) slices: direct differences, patched into the staged word
+    // ambiguous (row, codebook) slices: direct differences, patched into the staged words
     __syncwarp();
 #pragma unroll
-    for (int r = 0; r < kEnc2Rows; ++r) {
+    for (int r = 0; r < 2; ++r) {
         while (amb[r]) {
             const int c = __ffsll((long long)amb[r]) - 1;
             amb[r] &= amb[r] - 1;
-            const uint32_t arg =
-                direct_argmin<L>(reinterpret_cast<const float*>(xr[r]) + c * L, cneg + (size_t)c * L * kK);
-            const int pos = 4 * (2 * (threadIdx.x & 3) + r);  // nibble of this row in its group's word
-            uint32_t* w = stage + (threadIdx.x >> 2) * m + c;
+            const uint32_t arg = direct_argmin<L>(X + (row_blk + tid + 256 * r) * ldx + c * L, cneg + (size_t)c * L * kK);
+            const int pos = 4 * (tid & 7);
+            uint32_t* w = stage + ((tid + 256 * r) >> 3) * m + c;
             atomicAnd(w, ~(0xFu << pos));
             atomicOr(w, arg << pos);
         }
     }
-    __syncthreads();
-    const int64_t g0 = (int64_t)blockIdx.x * GPB;
+    asm volatile("bar.sync 1, %0;" ::"n"(kTmaWorkers) : "memory");
+    const int64_t g0 = (int64_t)blockIdx.x * (kTmaRows / kRowsPerWord);
     const int64_t groups = ceil_div(n, kRowsPerWord);
-    const int64_t ng = min64(GPB, groups - g0);
+    const int64_t ng = min64(kTmaRows / kRowsPerWord, groups - g0);
     uint32_t* dst = codes + g0 * m;
-    for (int64_t e = threadIdx.x; e < ng * m; e += blockDim.x) dst[e] = stage[e];
+    for (int64_t e = tid; e < ng * m; e += kTmaWorkers) dst[e] = stage[e];
 }
 
 __global__ void pack_kernel(const uint8_t* __restrict__ flat, int64_t n, int m,
@@ -495,30 +517,38 @@ __global__ void unpack_kernel(const uint32_t* __restrict__ codes, int64_t n, int
 }  // namespace
 
 cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,
-                          uint32_t* codes, int sms, cudaStream_t s, bool direct) {
+                          uint32_t* codes, int sms, cudaStream_t s, int mode) {
     if (n == 0) return cudaSuccess;
     const int L = j / m;
     size_t smem = (size_t)j * kK * sizeof(float) + (size_t)kEncGroupsPerBlock * m * sizeof(uint32_t);
     bool vec = (L % 4 == 0) && (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
     int64_t blocks = ceil_div(n, kEncRowsPerBlock);
+    if (mode == 2 && L == 8 && (ldx % 4) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && encode_tiled()) {
+        // TMA-staged expanded-distance kernel (bit-identical codes)
+        CUtensorMap xmap{};
+        const cuuint64_t dims[2] = {(cuuint64_t)j, (cuuint64_t)n};
+        const cuuint64_t strides[1] = {(cuuint64_t)(ldx * sizeof(float))};
+        const cuuint32_t box[2] = {(cuuint32_t)L, 256u};
+        const cuuint32_t estr[2] = {1u, 1u};
+        if (encode_tiled()(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+            const size_t tsmem = (size_t)kEncStages * kTmaRows * L * sizeof(float) + 2 * (size_t)j * kK * sizeof(float) +
+                                 (size_t)m * kK * sizeof(float) + (size_t)j * sizeof(float) +
+                                 (size_t)((m + 3) & ~3) * sizeof(float) +
+                                 ((size_t)(kTmaRows / kRowsPerWord) * m + 2) * sizeof(uint32_t) + 8 +
+                                 2 * kEncStages * sizeof(uint64_t);
+            cudaFuncSetAttribute(encode_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+            encode_tma_kernel<8><<<(unsigned)ceil_div(n, kTmaRows), kTmaWorkers + 32, tsmem, s>>>(xmap, X, n, ldx, C, m,
+                                                                                                codes);
+            return cudaGetLastError();
+        }
+    }
     if (vec && (L == 8 || L == 16) && (ldx % 8) == 0 && (reinterpret_cast<uintptr_t>(X) & 31) == 0) {
         static_assert(kEnc2RowsPerBlock == kEncRowsPerBlock, "same 64-group staging");
         const bool small = blocks < 2 * sms;  // halve the blocks' rows so that every SM gets work
-        // the expanded-distance kernel only on request (BOLT_ENCODE_EXPANDED) and
-        // for L = 8: it halves the FP32 work but measured slower (c2: 0.24 vs
-        // 0.20 ms; with less math per row slice the row-strided loads' latency
-        // is exposed -- DESIGN.md 6.3); L = 16 always takes the direct kernel
-        direct = direct || L != 8;
-        auto kern = direct ? (L == 8 ? (small ? encode_l8_kernel<8, 128> : encode_l8_kernel<8, 256>)
-                                     : (small ? encode_l8_kernel<16, 128> : encode_l8_kernel<16, 256>))
-                           : (small ? encode_fast_kernel<8, 128> : encode_fast_kernel<8, 256>);
-#ifdef BOLT_XMODE
-        if (!direct && getenv("BOLT_ENC_MINB3"))  // diagnostic A/B: 3 blocks per SM (85 registers)
-            kern = small ? encode_fast_kernel<8, 128, 3> : encode_fast_kernel<8, 256, 3>;
-#endif
-        if (!direct)  // -2c, ||c||^2, max |c| per dimension, the bound (encode_fast_kernel)
-            smem += (size_t)j * kK * sizeof(float) + (size_t)m * kK * sizeof(float) + (size_t)j * sizeof(float) +
-                    (size_t)((m + 3) & ~3) * sizeof(float);
+        auto kern = L == 8 ? (small ? encode_l8_kernel<8, 128> : encode_l8_kernel<8, 256>)
+                           : (small ? encode_l8_kernel<16, 128> : encode_l8_kernel<16, 256>);
         const int threads = small ? 128 : 256;
         const int64_t nb = ceil_div(n, (int64_t)threads * kEnc2Rows);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -574,8 +604,7 @@ cudaError_t launch_encode_append(const float* X, int64_t n_new, int j, int64_t l
         if (e != cudaSuccess) return e;
     }
     if (n_new == h) return cudaSuccess;
-    return launch_encode(X + h * ldx, n_new - h, j, ldx, C, m, codes + ((n_old + h) / kRowsPerWord) * m, sms, s,
-                         false);
+    return launch_encode(X + h * ldx, n_new - h, j, ldx, C, m, codes + ((n_old + h) / kRowsPerWord) * m, sms, s, 0);
 }
 
 cudaError_t launch_pack(const uint8_t* flat, int64_t n, int m, uint32_t* codes, cudaStream_t s) {

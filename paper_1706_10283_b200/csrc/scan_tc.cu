@@ -34,6 +34,7 @@
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
+#include "tma_host.cuh"
 #include "topk_list.cuh"
 
 namespace bolt {
@@ -1025,21 +1026,7 @@ cudaError_t launch_full_m(const ScanArgs& a, int rparts, FullOut fo, const CUten
                : launch_mk<M, false, 4, 1>(a, 1, 0, rparts, nullptr, nullptr, s, fo, omap);
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-inline EncodeTiledFn encode_tiled() {
-    static EncodeTiledFn fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            p = nullptr;
-        return reinterpret_cast<EncodeTiledFn>(p);
-    }();
-    return fn;
-}
+using bolt::encode_tiled;
 
 template <int M, bool kPairT>
 cudaError_t launch_mp(const ScanArgs& a, int k, int metric, int64_t index_base, int rparts, uint64_t* part_keys,
@@ -1110,12 +1097,12 @@ cudaError_t launch_scan_tc(const ScanArgs& a, uint16_t* out16, float* out32, int
     // layout; the hardware clips rows >= n and queries >= nq
     CUtensorMap omap{};
     int tma = 0;
-    if (vec && tc::encode_tiled()) {
+    if (vec && encode_tiled()) {
         const cuuint64_t dims[2] = {(cuuint64_t)a.nq, (cuuint64_t)a.n};
         const cuuint64_t strides[1] = {(cuuint64_t)(ldo * esz)};
         const cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)(32 / tc::kStorePieces)};  // a row slice of a warp's block
         const cuuint32_t estr[2] = {1u, 1u};
-        tma = tc::encode_tiled()(&omap, out32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, out,
+        tma = encode_tiled()(&omap, out32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, out,
                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }

@@ -82,7 +82,7 @@ def test_encode_centroid_identity(bolt, orc):
 
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_encode_fast_equals_direct_near_ties(bolt, orc, seed):
-    """The expanded-distance encoder (ENCODE_EXPANDED: ||c||^2 - 2 x.c ranking,
+    """The TMA-staged expanded-distance encoder (ENCODE_EXPANDED: ||c||^2 - 2 x.c ranking,
     rounding bound, direct fallback) returns the direct-difference kernel's
     codes bit for bit, on rows built at or near midpoints of centroid pairs
     (exact fp32 ties, 1e-5 .. 0.5 offsets) with c2-sized coordinates (0..255,
@@ -103,6 +103,10 @@ def test_encode_fast_equals_direct_near_ties(bolt, orc, seed):
     fast = host(bolt.encode(Xd, Cd, variant=bolt.ENCODE_EXPANDED))
     direct = host(bolt.encode(Xd, Cd, variant=bolt.ENCODE_DIRECT))
     np.testing.assert_array_equal(host(bolt.encode(Xd, Cd)), direct)
+    # ragged row counts (partial 512-row TMA blocks, partial groups)
+    for nn in (1, 7, 511, 513, 4099):
+        np.testing.assert_array_equal(host(bolt.encode(Xd[:nn], Cd, variant=bolt.ENCODE_EXPANDED)),
+                                      host(bolt.encode(Xd[:nn], Cd, variant=bolt.ENCODE_DIRECT)))
     np.testing.assert_array_equal(fast, direct)
     _encode_check(bolt, orc, X[:5000], C)
 

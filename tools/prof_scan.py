@@ -22,7 +22,8 @@ p.add_argument("--variant", default="prmt")
 p.add_argument("--what", default="topk")
 p.add_argument("--reps", type=int, default=2)
 p.add_argument("--prefill", action="store_true")
-p.add_argument("--direct", action="store_true", help="encode: the direct-difference kernel (else the expanded one)")
+p.add_argument("--direct", action="store_true", help="encode: the direct-difference kernel")
+p.add_argument("--expanded", action="store_true", help="encode: the register-loading expanded-distance kernel")
 p.add_argument("--config", default="", help="use a BASELINE config's real pipeline data (c2, c3)")
 a = p.parse_args()
 dev = torch.device("cuda")
@@ -79,7 +80,8 @@ def once():
     elif a.what == "dequant":
         bolt.scan_dequant(codes, a.n, ql, 0.5, 1.0, out=full_out, variant=v)
     elif a.what == "encode":
-        bolt.encode(X, C, variant=bolt.ENCODE_DIRECT if a.direct else bolt.ENCODE_EXPANDED)
+        bolt.encode(X, C, variant=bolt.ENCODE_DIRECT if a.direct else (bolt.ENCODE_EXPANDED if a.expanded
+                                                                         else bolt.ENCODE_AUTO))
 
 
 for _ in range(a.reps):
