@@ -118,10 +118,11 @@ TopkPlan topk_plan(int64_t n, int m, int64_t nq, int k, int variant, int sms) {
     p.ws = p.parts > 1 || p.small || v == BOLT_VARIANT_TCS || v == BOLT_VARIANT_SP
                ? (size_t)p.parts * nq * p.klist * sizeof(uint64_t) : 0;
     // shared per-query thresholds (u32) after the partial lists: PRMT one word,
-    // TC 9 nq + 4 (k-th value words + 16 B aligned rows of 8 union-group words, scan_tc.cu),
+    // TC 9 nq + 4 (k-th value words + 16 B aligned rows of 8 union-group words, scan_tc.cu;
+    // k > 32: 4 nq group words), then rparts ceil(nq / 128) finished-partition counters,
     // small-batch PRMT 33 nq (k-th value word + 32 minima slots, scan_small.cu)
     if (p.ws > 0)
-        p.ws += (size_t)(v == BOLT_VARIANT_TC ? (k > kTcListMax ? 4 * nq : 9 * nq + 4 + (p.parts / 2) * ceil_div(nq, 128))
+        p.ws += (size_t)(v == BOLT_VARIANT_TC ? (k > kTcListMax ? 4 * nq : 9 * nq + 4) + (p.parts / 2) * ceil_div(nq, 128)
                                               : p.small ? 33 * nq : nq) *
                 sizeof(uint32_t);  // TCS, SP: nq words; TC also the finished-partition counters [rparts][tiles_q]
     if (v == BOLT_VARIANT_TC && k > kTcListMax) {

@@ -101,6 +101,7 @@ constexpr int kPrefetch = 3;             // tiles of code words in flight per pr
 constexpr int kScratchStrideTopk = 20;
 constexpr int kScratchStrideFull = 32;
 constexpr int kUnionParts = 8;           // top-k: finished partitions whose lists seed a unit's bound
+constexpr int kGroupUnionParts = 16;     // ... lists of 32 (k > 32): sampled, so more lists pay
 constexpr int kUnionMinTiles = 256;      // ... only for units this long (the read costs ~50 tiles' time)
 constexpr int kUnionGroups = 2;          // top-k: groups of lists of the union bound (epilogue; 5 measured no better)
 static_assert(kUnionGroups == 2 || kUnionGroups == 5, "2 or 5 union groups (load widths)");
@@ -616,7 +617,9 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
         // for units of later waves, the exact k-th of 20-80 % of the rows,
         // much tighter than any single list's k-th.  Read once, at unit start.
         // (c2: scan 1.78 -> 1.73 ms)
-        uint32_t* done = gthr_inv + ((a.nq + 3) & ~int64_t(3)) + 8 * a.nq;  // [rparts][tiles_q]
+        // [rparts][tiles_q] after the threshold words (k <= 32: k-th words +
+        // union-group rows; lists of 32: the [nq][4] group words)
+        uint32_t* done = gthr_inv + (kGroup ? 4 * a.nq : ((a.nq + 3) & ~int64_t(3)) + 8 * a.nq);
         if (share && kOut == 0 && qvalid && part > 0 && ntiles >= kUnionMinTiles) {
             RegList<KMAX> ul;
             ul.init(k);
@@ -643,6 +646,38 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
             if (ul.v[KMAX - 1] != 0xFFFFFFFFu) {
                 const uint32_t tu = ul.v[KMAX - 1] - 1u;  // k-th smallest value of the union
                 asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gq), "r"(0xFFFFu - tu) : "memory");
+            }
+        }
+        // Lists of 32 (k > 32, R = 32 G rows needed): the same union, sampled --
+        // each finished list contributes its values at positions 4i + 3 (i < 8),
+        // each standing for 4 distinct rows at or below it, so the (R / 4)-th
+        // smallest sample bounds the R-th best value; folded into every group
+        // word (max_g min(G_g, T) = min(max_g G_g, T), still a valid bound).
+        if (kGroup && kOut == 0 && qvalid && part > 0 && ntiles >= kUnionMinTiles) {
+            RegList<32> ul;
+            ul.init(8 * ngrp);  // R / 4 = 8 G samples
+            for (int pp = 0; pp < min(part, kGroupUnionParts); ++pp) {
+                uint32_t dn;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(dn) : "l"(done + (int64_t)pp * tiles_q + tq));
+                if (dn != (kPairT ? 2u : 1u)) continue;
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const uint64_t* src = part_keys + ((int64_t)(2 * pp + hh) * a.nq + q0 + q) * k;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const uint64_t key = src[4 * i + 3];
+                        if (key == ~0ull) break;
+                        const uint32_t kv64 = (uint32_t)(key >> 48);
+                        const uint32_t kvp = kDot ? C::KVMAX - (0xFFFFu - kv64) : kv64;
+                        if (kvp + 1u >= ul.v[31]) break;  // sorted list: the rest is no better
+                        ul.insert(kvp + 1u);
+                    }
+                }
+            }
+            if (ul.v[31] != 0xFFFFFFFFu) {
+                const uint32_t tu = ul.v[31] - 1u;
+                for (int g = 0; g < ngrp; ++g)
+                    asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(gg + g), "r"(0xFFFFu - tu) : "memory");
             }
         }
         if (share) {
@@ -900,12 +935,11 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                 }
             }
         }
-        if (kOut == 0 && share) {
+        if (kOut == 0) {
             // this CTA's lists are written: count it in done[part][tq] (release)
             asm volatile("bar.sync 1, %0;" ::"n"(kEpilogue) : "memory");
             if (threadIdx.x == 0) {
                 __threadfence();
-                uint32_t* done = gthr_inv + ((a.nq + 3) & ~int64_t(3)) + 8 * a.nq;
                 atomicAdd(done + (int64_t)part * tiles_q + tq, 1u);
             }
         }
@@ -1006,8 +1040,9 @@ cudaError_t launch_mk(const ScanArgs& a, int k, int64_t index_base, int rparts, 
     if (kOut == 3) {  // swapped top-k: [nq] k-th-value words
         cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)a.nq * sizeof(uint32_t), s);
         if (e != cudaSuccess) return e;
-    } else if (kOut == 0 && kGroup) {  // large k: [nq][4] group words instead
-        cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)a.nq * 4 * sizeof(uint32_t), s);
+    } else if (kOut == 0 && kGroup) {  // large k: [nq][4] group words instead, then the done counters
+        const int64_t tq_count = ceil_div(a.nq, (kPairT ? 2 : 1) * C::QR);
+        cudaError_t e = cudaMemsetAsync(gthr, 0, (size_t)(a.nq * 4 + rparts * tq_count) * sizeof(uint32_t), s);
         if (e != cudaSuccess) return e;
     } else if (kOut == 0 && !(xmode & 16)) {  // diagnostic 16: keep caller-prefilled shared thresholds
         const int64_t hoff = (a.nq + 3) & ~int64_t(3);

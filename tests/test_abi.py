@@ -79,7 +79,7 @@ def test_workspace_sizing_host(lib):
     # (PRMT), 33 (small-batch PRMT kernel, nq < 64 and m in {8,16,32}: k-th
     # value + 32 minima slots), 9 nq + 4 + rparts ceil(nq / 128) (tcgen05: k-th
     # value words, 16 B aligned rows of 8 union-group words, finished-partition
-    # counters)
+    # counters; for k > 32 the 9 nq + 4 words become 4 nq group words)
     for n, m, nq, k, variant in [(10, 8, 4, 10, 1), (1_000_000, 16, 10_000, 10, 1), (10**8, 16, 1, 100, 1),
                                  (5000, 12, 8, 10, 1), (1_000_000, 16, 10_000, 10, 2), (777, 32, 300, 32, 2)]:
         ws = lib.bolt_topk_workspace_bytes_ex(n, m, nq, k, variant)
