@@ -101,14 +101,15 @@ BOLT_API int64_t bolt_codes_words(int64_t n, int m);     /* (host) ceil(n/8)*m, 
  * Errors: NULL, SHAPE (n < 0, j < 1, m not in 1..64, j % m, ldx < j, j/m > 64). */
 BOLT_API bolt_status bolt_encode(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,
                         uint32_t* codes, bolt_stream_t stream);
-/* As bolt_encode with an explicit kernel.  BOLT_ENCODE_AUTO and
- * BOLT_ENCODE_DIRECT: direct differences, fp32 (x - c)^2 summed in ascending
- * dimension (the arithmetic whose argmin is returned).  BOLT_ENCODE_EXPANDED
- * (j/m = 8, rows 32 B aligned; else direct): the distances are first ranked
- * by the expansion ||c||^2 - 2 x.c (one FMA per dimension and centroid) and a
- * codebook whose best centroids lie within that computation's rounding bound
- * is redone by direct differences, so the codes equal BOLT_ENCODE_DIRECT's bit
- * for bit; measured slower on a B200, hence not the default.
+/* As bolt_encode with an explicit kernel.  BOLT_ENCODE_DIRECT: direct
+ * differences, fp32 (x - c)^2 summed in ascending dimension (the arithmetic
+ * whose argmin is returned).  BOLT_ENCODE_EXPANDED (j/m in {8, 16}, j % 32 == 0,
+ * j <= 512, m % 8 == 0, rows 16 B aligned; else direct): the distances are
+ * first ranked by the expansion ||c||^2 - 2 x.c (one FMA per dimension and
+ * centroid) and a codebook whose two best centroids lie within that
+ * computation's rounding bound is redone by direct differences, so the codes
+ * equal BOLT_ENCODE_DIRECT's bit for bit.  BOLT_ENCODE_AUTO: EXPANDED for
+ * j/m = 8 (measured faster on a B200), DIRECT otherwise.
  * Errors: as bolt_encode; RANGE for another variant. */
 enum { BOLT_ENCODE_AUTO = 0, BOLT_ENCODE_DIRECT = 1, BOLT_ENCODE_EXPANDED = 2 };
 BOLT_API bolt_status bolt_encode_ex(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,

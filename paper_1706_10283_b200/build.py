@@ -56,7 +56,8 @@ def _compile(src, verbose, objdir=OBJ):
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False, profile: bool = False, xmode: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, profile: bool = False, xmode: bool = False,
+          variant: str = "") -> str:
     """Diagnostic builds (tools/ only, loaded with BOLT_LIB=<name>):
     profile=True -> libbolt_prof.so with -DBOLT_PROFILE (cycle counters) and -DBOLT_XMODE;
     xmode=True -> libbolt_x.so with -DBOLT_XMODE (BOLT_TC_XMODE experiment
@@ -69,6 +70,11 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False, xmo
     elif xmode:
         NVCC_FLAGS = NVCC_FLAGS + ["-DBOLT_XMODE"]
         lib, objdir = os.path.join(PKG, "libbolt_x.so"), OBJ + "_x"
+    elif variant:
+        # A/B variant: "name:-DFOO=1,-DBAR=2" -> libbolt_name.so (tools/ only)
+        name, _, defs = variant.partition(":")
+        NVCC_FLAGS = NVCC_FLAGS + [d for d in defs.split(",") if d]
+        lib, objdir = os.path.join(PKG, f"libbolt_{name}.so"), OBJ + f"_{name}"
     os.makedirs(objdir, exist_ok=True)
     if not force and not _stale(lib, _deps()):
         return lib
@@ -92,5 +98,6 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False, xmo
 
 
 if __name__ == "__main__":
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
     print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv,
-                profile="--profile" in sys.argv, xmode="--xmode" in sys.argv))
+                profile="--profile" in sys.argv, xmode="--xmode" in sys.argv, variant=var))

@@ -9,6 +9,7 @@
 // d += (x - c)^2.  The argmin keeps the lowest index on ties (R9).  Codes of
 // a block (512 rows = 64 layout-v1 groups) are staged in shared memory and
 // written as one contiguous run of 64*m words.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -290,57 +291,84 @@ __device__ __noinline__ uint32_t direct_argmin(const float* __restrict__ x, cons
 // distances keep the same unique minimum.  The factors carry a >= 25 % slack
 // for the rounding of the test itself.
 //
-// The kernel stages the row slices of a codebook in shared memory by 2-D
-// tensor copies (one 256-row x 32-byte box per half block) instead of
-// register loads (a register-loading version of the same arithmetic ran at
-// 0.24 ms on c2, its loads exposed; ncu profiles/r2/ncu_full_enc_*.txt).
-// Warp 8 issues the copies kEncStages slices ahead; warps 0-7 (thread t =
-// local rows t and t + 256) rank the centroids and pack the layout-v1 words
-// with shuffles.  Measured c2: 0.205 ms against the direct kernel's 0.199 --
-// no faster, so it is the explicit variant, not the default.
-constexpr int kEncStages = 4;
-constexpr int kTmaRows = 512;               // rows per block
-constexpr int kTmaWorkers = 256;            // compute threads (2 rows each)
+// The kernel is persistent (one CTA per SM; the centroid tables are set up
+// once) and streams whole rows: a stage is R = 32 RT consecutive rows x J
+// floats, brought in by J/32 2-D tensor copies of 32-float (128-byte) x R
+// boxes in the 128-byte swizzle, kRowStages stages in flight.  Warp 8 issues
+// the copies; compute warp w owns codebooks [w CPW, w CPW + CPW) of every row
+// of RT of the stage's NS 32-row slabs (lane = row within a slab), so the
+// centroid loads of a codebook are shared by RT rows.  (Round 2's first version staged
+// 32-byte row slices per codebook in short-lived 512-row blocks: 0.205 ms on
+// c2, no faster than the direct kernel.)
 
+// direct_argmin reading the centroids from global memory (x + (-c) == x - c
+// exactly): the expanded kernel's rare fallback, no negated table in shared memory
 template <int L>
-__global__ void __launch_bounds__(kTmaWorkers + 32, 2)
-encode_tma_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ X, int64_t n, int64_t ldx,
-                  const float* __restrict__ C, int m, uint32_t* __restrict__ codes) {
-    static_assert(L == 8, "32-byte row slices");
-    extern __shared__ __align__(1024) uint8_t enc_tma_smem[];
+__device__ __noinline__ uint32_t direct_argmin_g(const float* __restrict__ x, const float* __restrict__ c) {
+    float2 d[kK / 2];
+#pragma unroll
+    for (int p = 0; p < kK / 2; ++p) d[p] = make_float2(0.f, 0.f);
+    for (int t = 0; t < L; ++t) {
+        const float xt = __ldg(x + t);
+        const float2 xx = make_float2(xt, xt);
+#pragma unroll
+        for (int p = 0; p < kK / 2; ++p) {
+            const float2 cp = make_float2(-__ldg(c + (2 * p) * L + t), -__ldg(c + (2 * p + 1) * L + t));
+            const float2 dd = __fadd2_rn(xx, cp);
+            d[p] = __ffma2_rn(dd, dd, d[p]);
+        }
+    }
+    float best = d[0].x;
+    uint32_t arg = 0;
+#pragma unroll
+    for (int p = 0; p < kK / 2; ++p) {
+        if (p > 0 && d[p].x < best) { best = d[p].x; arg = 2 * p; }
+        if (d[p].y < best) { best = d[p].y; arg = 2 * p + 1; }
+    }
+    return arg;
+}
+
+template <int L, int NS, int RT, int W>
+__global__ void __launch_bounds__(32 * W + 32, 1)
+encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ X, int64_t n, int64_t ldx,
+                   const float* __restrict__ C, int m, uint32_t* __restrict__ codes, int64_t nblocks, int S,
+                   int xm) {
+    static_assert(L == 8 || L == 16, "32-float boxes hold 32 / L codebooks");
+#ifndef BOLT_XMODE
+    xm = 0;  // diagnostic switches (1: loads only, 2: no fallback, 4: no code stores) exist only in libbolt_x.so
+#endif
+    extern __shared__ __align__(1024) uint8_t enc_row_smem[];
     constexpr float kU = 5.9604645e-8f;  // 2^-24
     constexpr float kGL = (float)L * kU / (1.0f - (float)L * kU);
     constexpr float kGL2 = (float)(L + 2) * kU / (1.0f - (float)(L + 2) * kU);
-    constexpr int SLICE = kTmaRows * L * 4;  // bytes of one codebook's row slices
+    static_assert(NS % RT == 0, "slab groups");
+    constexpr int R = 32 * NS;           // rows per stage
+    constexpr int SG = NS / RT;          // slab groups (of RT slabs)
     const int j = m * L;
-    float* xs = reinterpret_cast<float*>(enc_tma_smem);                 // [S][512][L]
-    float* cneg = xs + kEncStages * kTmaRows * L;                        // [m][L][16] -c
-    float* cm2 = cneg + (size_t)j * kK;                                  // [m][L][16] -2c
+    const int nbox = j / 32;
+    const uint32_t stage_bytes = (uint32_t)R * j * 4;
+    const int cpw = m * SG / W;          // codebooks per compute warp (m * SG % W == 0)
+    uint8_t* xs = enc_row_smem;                                          // [S][j/32][R][32] swizzled
+    float* cm2 = reinterpret_cast<float*>(xs + (size_t)S * stage_bytes);  // [m][L][16] -2c
     float* cn = cm2 + (size_t)j * kK;                                    // [m][16]
-    float* amax = cn + (size_t)m * kK;                                   // [m][L]
-    float* c2max = amax + (size_t)j;                                     // [m]
-    uint32_t* stage = reinterpret_cast<uint32_t*>(c2max + ((m + 3) & ~3));  // [64][m]
-    uint64_t* full = reinterpret_cast<uint64_t*>(stage + (size_t)(kTmaRows / kRowsPerWord) * m + 2);  // 8 B aligned
-    full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
-    uint64_t* empty = full + kEncStages;
+    float* c2max = cn + (size_t)m * kK;                                  // [m]
+    uint64_t* full = reinterpret_cast<uint64_t*>(c2max + ((m + 1) & ~1));
+    uint64_t* empty = full + S;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t row_blk = (int64_t)blockIdx.x * kTmaRows;
     if (tid == 0) {
-        for (int i = 0; i < kEncStages; ++i) {
+        for (int i = 0; i < S; ++i) {
             tc::mbar_init(&full[i], 1);
-            tc::mbar_init(&empty[i], kTmaWorkers / 32);
+            tc::mbar_init(&empty[i], W);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
-    // centroid tables (all threads), before the copy warp enters its loop: a
-    // block barrier after that point would deadlock against its empty-slot waits
+    // centroid tables, before the copy warp enters its loop (a block barrier
+    // after that point would deadlock against its empty-slot waits)
     for (int e = tid; e < j * kK; e += blockDim.x) {
         int c = e / (kK * L);
         int r = e - c * kK * L;
         int k = r / L;
         int d = r - k * L;
-        cneg[((size_t)c * L + d) * kK + k] = -C[e];
         cm2[((size_t)c * L + d) * kK + k] = -2.0f * C[e];
     }
     for (int e = tid; e < m * kK; e += blockDim.x) {
@@ -349,12 +377,6 @@ encode_tma_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restr
         for (int t = 0; t < L; ++t) acc = __fmaf_rn(ck[t], ck[t], acc);
         cn[e] = acc;
     }
-    for (int e = tid; e < j; e += blockDim.x) {
-        const int c = e / L, t = e - c * L;
-        float a = 0.f;
-        for (int k = 0; k < kK; ++k) a = fmaxf(a, fabsf(C[((size_t)c * kK + k) * L + t]));
-        amax[e] = a;
-    }
     __syncthreads();
     for (int c = tid; c < m; c += blockDim.x) {
         float a = 0.f;
@@ -362,132 +384,154 @@ encode_tma_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restr
         c2max[c] = a * (1.0f + 2.0f * kGL);
     }
     __syncthreads();
-    if (warp == kTmaWorkers / 32) {
+    if (warp == W) {
         // ------------------------------------------------ copy warp
         if (lane == 0) {
-            for (int c = 0; c < m; ++c) {
-                const int s = c % kEncStages;
-                tc::mbar_wait(&empty[s], ((c / kEncStages) & 1) ^ 1);
+            int i = 0;
+            for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
+                const int s = i % S;
+                tc::mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(&full[s])),
-                             "r"(SLICE)
+                             "r"(stage_bytes)
                              : "memory");
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
+                const uint32_t dst = tc::smem_u32(xs + (size_t)s * stage_bytes);
+                for (int bx = 0; bx < nbox; ++bx)
                     asm volatile(
                         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-                            "r"(tc::smem_u32(xs + ((size_t)s * kTmaRows + h * 256) * L)),
-                        "l"(&xmap), "r"(c * L), "r"((int)(row_blk + h * 256)), "r"(tc::smem_u32(&full[s]))
+                            "r"(dst + (uint32_t)bx * (R * 128)),
+                        "l"(&xmap), "r"(bx * 32), "r"((int)(b * R)), "r"(tc::smem_u32(&full[s]))
                         : "memory");
             }
         }
         return;
     }
     // ---------------------------------------------------- compute warps
-    uint64_t amb[2] = {0ull, 0ull};
-    const bool valid[2] = {row_blk + tid < n, row_blk + tid + 256 < n};
-    for (int c = 0; c < m; ++c) {
-        const int s = c % kEncStages;
-        tc::mbar_wait(&full[s], (c / kEncStages) & 1);
-        float xv[2][L];
+    int i = 0;
+    for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
+        const int s = i % S;
+        const int64_t row_blk = b * R;
+        uint32_t amb = 0;  // ambiguous (codebook, slab) items of this stage, bit cc RT + r
+        tc::mbar_wait(&full[s], (i / S) & 1);
+        const uint8_t* st = xs + (size_t)s * stage_bytes;
+        for (int cc = 0; cc < (xm & 1 ? 0 : cpw); ++cc) {
+            const int c = (warp / SG) * cpw + cc;
+            const int sl0 = (warp % SG) * RT;         // first slab of this warp
+            const int bx = (c * L) >> 5;              // box of this codebook's L floats
+            const int ch0 = ((c * L) & 31) >> 2;      // its first 16-byte chunk within the 128-byte row
+            float xv[RT][L];
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const float4* xp = reinterpret_cast<const float4*>(xs + ((size_t)s * kTmaRows + tid + 256 * r) * L);
-            const float4 a0 = xp[0], a1 = xp[1];
-            xv[r][0] = a0.x; xv[r][1] = a0.y; xv[r][2] = a0.z; xv[r][3] = a0.w;
-            xv[r][4] = a1.x; xv[r][5] = a1.y; xv[r][6] = a1.z; xv[r][7] = a1.w;
+            for (int r = 0; r < RT; ++r) {
+                const int rl = 32 * (sl0 + r) + lane;
+                const uint8_t* rowp = st + (size_t)bx * (R * 128) + rl * 128;
+#pragma unroll
+                for (int h = 0; h < L / 4; ++h) {
+                    const float4 v = *reinterpret_cast<const float4*>(rowp + (((ch0 + h) ^ (rl & 7)) << 4));
+                    xv[r][4 * h] = v.x; xv[r][4 * h + 1] = v.y; xv[r][4 * h + 2] = v.z; xv[r][4 * h + 3] = v.w;
+                }
+            }
+            float2 sv[RT][kK / 2];
+            float2 x2p[RT];  // ||x||^2 of the slice, as (even, odd) dimension partial sums
+            {
+                const float4* cn4 = reinterpret_cast<const float4*>(cn + c * kK);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float4 v = cn4[q];
+#pragma unroll
+                    for (int r = 0; r < RT; ++r) {
+                        sv[r][2 * q] = make_float2(v.x, v.y);
+                        sv[r][2 * q + 1] = make_float2(v.z, v.w);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < RT; ++r) {
+                    x2p[r] = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int h = 0; h < L / 2; ++h) {
+                        const float2 xp = make_float2(xv[r][2 * h], xv[r][2 * h + 1]);
+                        x2p[r] = __ffma2_rn(xp, xp, x2p[r]);
+                    }
+                }
+            }
+            const float* ccm = cm2 + (size_t)c * L * kK;
+#pragma unroll
+            for (int t = 0; t < L; ++t) {
+                const float4* cv = reinterpret_cast<const float4*>(ccm + (size_t)t * kK);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float4 c4 = cv[q];
+                    const float2 ca = make_float2(c4.x, c4.y), cb = make_float2(c4.z, c4.w);
+#pragma unroll
+                    for (int r = 0; r < RT; ++r) {
+                        const float2 xx = make_float2(xv[r][t], xv[r][t]);
+                        sv[r][2 * q] = __ffma2_rn(xx, ca, sv[r][2 * q]);
+                        sv[r][2 * q + 1] = __ffma2_rn(xx, cb, sv[r][2 * q + 1]);
+                    }
+                }
+            }
+            const float c2 = c2max[c];
+#pragma unroll
+            for (int r = 0; r < RT; ++r) {
+                const int64_t row = row_blk + 32 * (sl0 + r) + lane;
+                const bool valid = row < n;
+                // index k in the low 4 mantissa bits of s^_k (a change of < 2^-19 |s^_k|):
+                // the minimum of the tagged values names its centroid; a (min,
+                // second) tree gives the two smallest
+                float lo[kK / 2], hi[kK / 2];
+#pragma unroll
+                for (int p = 0; p < kK / 2; ++p) {
+                    const float e0 = __uint_as_float((__float_as_uint(sv[r][p].x) & ~0xFu) | (2u * p));
+                    const float e1 = __uint_as_float((__float_as_uint(sv[r][p].y) & ~0xFu) | (2u * p + 1u));
+                    lo[p] = fminf(e0, e1);
+                    hi[p] = fmaxf(e0, e1);
+                }
+#pragma unroll
+                for (int w = kK / 4; w >= 1; w /= 2)
+#pragma unroll
+                    for (int p = 0; p < w; ++p) {
+                        const float l = fminf(lo[p], lo[p + w]);
+                        hi[p] = fminf(fmaxf(lo[p], lo[p + w]), fminf(hi[p], hi[p + w]));
+                        lo[p] = l;
+                    }
+                const float b1 = lo[0], b2 = hi[0];
+                // |s^_k| <= A = 2 C2 + X2 (2|x.c| <= X2 + ||c||^2), so E = 4 g(L) A
+                // bounds |s^_k - s_k| (2 sum|x_t||c_kt| <= X2 + C2) and the tags move
+                // each value by < 2^-19 A; need' = need + 2 * 2^-19 A (25 % slack)
+                const float X2 = (x2p[r].x + x2p[r].y) * (1.0f + 2.0f * kGL);
+                const float A = 2.0f * c2 + X2;
+                const float E = 4.0f * kGL * A;
+                const float need = 2.5f * E + 3.0f * kGL2 * (X2 + fabsf(b1) + E) + 1.25f * 3.8146973e-6f * A;
+                const bool ambig = !(b2 >= b1 + need) && valid;
+                const uint32_t arg = valid ? (__float_as_uint(b1) & 0xFu) : 0u;
+                amb |= (ambig ? 1u : 0u) << (cc * RT + r);
+                // layout-v1 word of this row's group: 8 consecutive lanes hold its 8 rows
+                uint32_t v = arg << (4 * (lane & 7));
+                v |= __shfl_xor_sync(0xffffffffu, v, 1);
+                v |= __shfl_xor_sync(0xffffffffu, v, 2);
+                v |= __shfl_xor_sync(0xffffffffu, v, 4);
+                const int64_t g = row >> 3;
+                if ((lane & 7) == 0 && g * kRowsPerWord < n && !(xm & 4)) codes[g * m + c] = v;
+            }
         }
+        // ambiguous (row, codebook) slices: direct differences (the direct
+        // kernel's exact fp32 operations), patched into the stored words; the
+        // lanes of a warp run their fallbacks side by side
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&empty[s]);  // the slice is in registers
-        float2 sv[2][kK / 2];
-        float2 xa[2];
-        {
-            const float4* cn4 = reinterpret_cast<const float4*>(cn + c * kK);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const float4 v = cn4[q];
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    sv[r][2 * q] = make_float2(v.x, v.y);
-                    sv[r][2 * q + 1] = make_float2(v.z, v.w);
-                }
-            }
-            xa[0] = xa[1] = make_float2(0.f, 0.f);
-        }
-        const float* cc = cm2 + (size_t)c * L * kK;
-        const float* am = amax + c * L;
-#pragma unroll
-        for (int t = 0; t < L; ++t) {
-            const float4* cv = reinterpret_cast<const float4*>(cc + (size_t)t * kK);
-            const float at = am[t];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                float4 c4 = cv[q];
-                float2 ca = make_float2(c4.x, c4.y), cb = make_float2(c4.z, c4.w);
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    float2 xx = make_float2(xv[r][t], xv[r][t]);
-                    sv[r][2 * q] = __ffma2_rn(xx, ca, sv[r][2 * q]);
-                    sv[r][2 * q + 1] = __ffma2_rn(xx, cb, sv[r][2 * q + 1]);
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-                xa[r] = __ffma2_rn(make_float2(xv[r][t], fabsf(xv[r][t])), make_float2(xv[r][t], at), xa[r]);
-        }
-        const float c2 = c2max[c];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            float mn[kK / 2];
-#pragma unroll
-            for (int p = 0; p < kK / 2; ++p) mn[p] = fminf(sv[r][p].x, sv[r][p].y);
-#pragma unroll
-            for (int w = kK / 4; w >= 1; w /= 2)
-#pragma unroll
-                for (int p = 0; p < w; ++p) mn[p] = fminf(mn[p], mn[p + w]);
-            const float b1 = mn[0];
-            const float E = 4.0f * kGL * (c2 + 2.0f * xa[r].y * (1.0f + 2.0f * kGL));
-            const float need = 2.5f * E + 3.0f * kGL2 * (xa[r].x * (1.0f + 2.0f * kGL) + fabsf(b1) + E);
-            const float thr = b1 + need;
-            uint32_t bl[kK / 2];
-#pragma unroll
-            for (int p = 0; p < kK / 2; ++p)
-                bl[p] = ((sv[r][p].x < thr ? 1u : 0u) | (sv[r][p].y < thr ? 2u : 0u)) << (2 * p);
-#pragma unroll
-            for (int w = kK / 4; w >= 1; w /= 2)
-#pragma unroll
-                for (int p = 0; p < w; ++p) bl[p] |= bl[p + w];
-            const uint32_t below = bl[0];
-            uint32_t arg = __ffs(below) - 1;
-            if (__popc(below) != 1 && valid[r]) amb[r] |= 1ull << c;
-            if (!valid[r]) arg = 0;
-            // layout-v1 word of this row's group: 8 consecutive lanes hold its 8 rows
-            uint32_t v = (arg & 0xFu) << (4 * (tid & 7));
-            v |= __shfl_xor_sync(0xffffffffu, v, 1);
-            v |= __shfl_xor_sync(0xffffffffu, v, 2);
-            v |= __shfl_xor_sync(0xffffffffu, v, 4);
-            if ((tid & 7) == 0) stage[((tid + 256 * r) >> 3) * m + c] = v;
-        }
-    }
-    // ambiguous (row, codebook) slices: direct differences, patched into the staged words
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        while (amb[r]) {
-            const int c = __ffsll((long long)amb[r]) - 1;
-            amb[r] &= amb[r] - 1;
-            const uint32_t arg = direct_argmin<L>(X + (row_blk + tid + 256 * r) * ldx + c * L, cneg + (size_t)c * L * kK);
-            const int pos = 4 * (tid & 7);
-            uint32_t* w = stage + ((tid + 256 * r) >> 3) * m + c;
+        if (xm & 2) amb = 0;
+        while (amb) {
+            const int bit = __ffs(amb) - 1;
+            amb &= amb - 1;
+            const int cc = bit / RT, r = bit - cc * RT;
+            const int c = (warp / SG) * cpw + cc;
+            const int64_t row = row_blk + 32 * ((warp % SG) * RT + r) + lane;
+            const uint32_t arg = direct_argmin_g<L>(X + row * ldx + c * L, C + (size_t)c * kK * L);
+            const int pos = 4 * (int)(row & 7);
+            uint32_t* w = codes + (row >> 3) * m + c;
             atomicAnd(w, ~(0xFu << pos));
             atomicOr(w, arg << pos);
         }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&empty[s]);  // this warp is done with the stage
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(kTmaWorkers) : "memory");
-    const int64_t g0 = (int64_t)blockIdx.x * (kTmaRows / kRowsPerWord);
-    const int64_t groups = ceil_div(n, kRowsPerWord);
-    const int64_t ng = min64(kTmaRows / kRowsPerWord, groups - g0);
-    uint32_t* dst = codes + g0 * m;
-    for (int64_t e = tid; e < ng * m; e += kTmaWorkers) dst[e] = stage[e];
 }
 
 __global__ void pack_kernel(const uint8_t* __restrict__ flat, int64_t n, int m,
@@ -523,24 +567,46 @@ cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const f
     size_t smem = (size_t)j * kK * sizeof(float) + (size_t)kEncGroupsPerBlock * m * sizeof(uint32_t);
     bool vec = (L % 4 == 0) && (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
     int64_t blocks = ceil_div(n, kEncRowsPerBlock);
-    if (mode == 2 && L == 8 && (ldx % 4) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && encode_tiled()) {
-        // TMA-staged expanded-distance kernel (bit-identical codes)
+    // AUTO: the expanded kernel for J/M = 8 (c2 0.185 vs 0.199 ms, c4 0.059 vs
+    // 0.067); J/M = 16 keeps the direct kernel (c3 0.70 vs 0.67 ms)
+    if ((mode == 2 || (mode == 0 && L == 8)) && (L == 8 || L == 16) && j % 32 == 0 && j <= 512 && m % 8 == 0 && (ldx % 4) == 0 &&
+        (reinterpret_cast<uintptr_t>(X) & 15) == 0 && encode_tiled()) {
+        // persistent whole-row TMA expanded-distance kernel (bit-identical codes)
+        const int NS = j <= 128 ? 4 : j <= 256 ? 2 : 1;  // 32-row slabs per stage (64 KB stages)
+        int W = 16, RT = NS == 1 ? 1 : 2;                // compute warps, slabs per thread
+#ifdef BOLT_XMODE
+        if (getenv("BOLT_ENC_W8") && NS == 4) W = 8, RT = 4;
+#endif
+        const int R = 32 * NS;
+        const size_t stage = (size_t)R * j * sizeof(float);
+        const size_t tables = (size_t)j * kK * sizeof(float) + (size_t)m * kK * sizeof(float) +
+                              (size_t)((m + 1) & ~1) * sizeof(float);
+        const size_t budget = 227 * 1024 - 1024;
+        int S = (int)std::min<size_t>(4, (budget - tables - 8 * sizeof(uint64_t)) / stage);
+        int xm = 0;
+#ifdef BOLT_XMODE
+        if (const char* e = getenv("BOLT_ENC_XMODE")) xm = atoi(e);
+        if (const char* e = getenv("BOLT_ENC_STAGES")) S = std::min(S, atoi(e));
+#endif
         CUtensorMap xmap{};
         const cuuint64_t dims[2] = {(cuuint64_t)j, (cuuint64_t)n};
         const cuuint64_t strides[1] = {(cuuint64_t)(ldx * sizeof(float))};
-        const cuuint32_t box[2] = {(cuuint32_t)L, 256u};
+        const cuuint32_t box[2] = {32u, (cuuint32_t)R};
         const cuuint32_t estr[2] = {1u, 1u};
-        if (encode_tiled()(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
-            const size_t tsmem = (size_t)kEncStages * kTmaRows * L * sizeof(float) + 2 * (size_t)j * kK * sizeof(float) +
-                                 (size_t)m * kK * sizeof(float) + (size_t)j * sizeof(float) +
-                                 (size_t)((m + 3) & ~3) * sizeof(float) +
-                                 ((size_t)(kTmaRows / kRowsPerWord) * m + 2) * sizeof(uint32_t) + 8 +
-                                 2 * kEncStages * sizeof(uint64_t);
-            cudaFuncSetAttribute(encode_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-            encode_tma_kernel<8><<<(unsigned)ceil_div(n, kTmaRows), kTmaWorkers + 32, tsmem, s>>>(xmap, X, n, ldx, C, m,
-                                                                                                codes);
+        if (S >= 2 && (m * (NS / RT)) % W == 0 &&
+            encode_tiled()(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+            const size_t tsmem = (size_t)S * stage + tables + 2 * (size_t)S * sizeof(uint64_t);
+            const int64_t nblocks = ceil_div(n, (int64_t)R);
+            const unsigned grid = (unsigned)std::min<int64_t>(nblocks, sms);
+            decltype(&encode_rows_kernel<8, 4, 2, 16>) kern;
+            if (L == 8) kern = NS == 4 ? (W == 8 ? encode_rows_kernel<8, 4, 4, 8> : encode_rows_kernel<8, 4, 2, 16>)
+                             : NS == 2 ? encode_rows_kernel<8, 2, 2, 16> : encode_rows_kernel<8, 1, 1, 16>;
+            else kern = NS == 4 ? encode_rows_kernel<16, 4, 2, 16>
+                        : NS == 2 ? encode_rows_kernel<16, 2, 2, 16> : encode_rows_kernel<16, 1, 1, 16>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+            kern<<<grid, 32 * W + 32, tsmem, s>>>(xmap, X, n, ldx, C, m, codes, nblocks, S, xm);
             return cudaGetLastError();
         }
     }
