@@ -478,6 +478,8 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
         constexpr int NW4 = MH / 4;                 // uint4 loads per vector
         constexpr int ch = 0;
         const uint32_t sh = (t & 7) * 4;            // kProducers % 8 == 0: the same for every vector of t
+        // 8 * code = bits 3..6 of the word rotated right by sh - 3 (one funnel shift + mask)
+        const uint32_t rot = (sh - 3u) & 31u;
         auto load_words = [&](int tile, uint4 (&w)[VPT][NW4]) {
 #pragma unroll
             for (int u = 0; u < VPT; ++u) {
@@ -510,7 +512,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
 #pragma unroll
                         for (int j = 0; j < 4 && 4 * i + j < MH; ++j)
                             *reinterpret_cast<uint4*>(b + (4 * i + j) * (C::NH * 16)) =
-                                one_hot16_s(((ws[j] >> sh) & 0xFu) * 8u);
+                                one_hot16_s(__funnelshift_r(ws[j], ws[j], rot) & 0x78u);
                     }
                 } else {  // last, partial tile: rows past the range are all-zero
                     const bool valid = hb + v < vend;
@@ -520,7 +522,7 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
 #pragma unroll
                         for (int j = 0; j < 4 && 4 * i + j < MH; ++j)
                             *reinterpret_cast<uint4*>(b + (4 * i + j) * (C::NH * 16)) =
-                                one_hot16_s(valid ? ((ws[j] >> sh) & 0xFu) * 8u : 128u);
+                                one_hot16_s(valid ? (__funnelshift_r(ws[j], ws[j], rot) & 0x78u) : 128u);
                     }
                 }
             }

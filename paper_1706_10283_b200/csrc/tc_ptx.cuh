@@ -155,9 +155,18 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t s) {
     asm("shl.b32 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(s));
     return d;
 }
-// one-hot of a 4-bit code as 16 bytes: byte `code` = 1 (s = 8 * code)
+// one-hot of a 4-bit code as 16 bytes: byte `code` = 1 (s = 8 * code).
+// Two clamped 64-bit shifts (amounts >= 64, including s - 64 wrapped for
+// s < 64, give 0): one address add instead of three.
 __device__ __forceinline__ uint4 one_hot16_s(uint32_t s) {
+#ifdef BOLT_ONEHOT32
     return make_uint4(shl_clamp(1u, s), shl_clamp(1u, s - 32u), shl_clamp(1u, s - 64u), shl_clamp(1u, s - 96u));
+#else
+    uint64_t lo, hi;
+    asm("shl.b64 %0, %1, %2;" : "=l"(lo) : "l"(1ull), "r"(s));
+    asm("shl.b64 %0, %1, %2;" : "=l"(hi) : "l"(1ull), "r"(s - 64u));
+    return make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
+#endif
 }
 
 __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
