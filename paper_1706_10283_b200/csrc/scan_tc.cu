@@ -106,6 +106,9 @@ constexpr int kUnionMinTiles = 256;      // ... only for units this long (the re
 constexpr int kUnionGroups = 2;          // top-k: groups of lists of the union bound (epilogue; 5 measured no better)
 static_assert(kUnionGroups == 2 || kUnionGroups == 5, "2 or 5 union groups (load widths)");
 constexpr int kStorePieces = 2;          // full output: TMA stores per 32-row x 128-byte warp block
+#ifndef BOLT_TC_STORE_HINT
+#define BOLT_TC_STORE_HINT 1  // evict-first L2 policy on the full-output TMA stores (c4 u16 0.066 -> 0.059 ms, fp32 0.090 -> 0.087)
+#endif
 
 // QROWS: query rows of the table buffer per CTA (kQM, or kNQ/2 in the
 // swapped top-k); LIST_BYTES: the swapped top-k's per-warp lists (else the
@@ -216,9 +219,18 @@ struct FullOut {
 };
 
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem, int x, int y) {
+#if BOLT_TC_STORE_HINT
+    // evict-first L2 policy for the streamed output (drains in issue order)
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(map),
+                 "r"(smem), "r"(x), "r"(y), "l"(pol)
+                 : "memory");
+#else
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
                  "r"(smem), "r"(x), "r"(y)
                  : "memory");
+#endif
 }
 
 // ------------------------------------------------ swapped top-k epilogue

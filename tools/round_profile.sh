@@ -29,3 +29,13 @@ python tools/prof_scan.py --variant sp --reps 2 --config c2 > gpurun_out/p5.txt 
   ncu --set full --clock-control none --import-source on -k regex:topk_sp -s 2 -c 1 -o gpurun_out/sp_c2 -f \
   python tools/prof_scan.py --variant sp --reps 2 --config c2 > gpurun_out/ncu_sp.log 2>&1
 python bench.py --config c5 --steps 3 --warmup 3 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
+python tools/prof_scan.py --what encode --reps 2 --config c2 > gpurun_out/p6.txt 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:encode -s 1 -c 1 -o gpurun_out/enc_c2 -f \
+  python tools/prof_scan.py --what encode --reps 1 --config c2 > gpurun_out/ncu_enc.log 2>&1
+# summaries on the box (the .ncu-rep files would exceed gpurun's 64 MiB copy-back)
+for r in gpurun_out/*.ncu-rep; do
+  b=${r%.ncu-rep}
+  python tools/ncu_summary.py $r > $b.summary.txt 2>&1
+  python tools/ncu_regions.py $r 0.005 > $b.regions.txt 2>&1
+  rm -f $r
+done
