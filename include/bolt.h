@@ -108,8 +108,8 @@ BOLT_API bolt_status bolt_encode(const float* X, int64_t n, int j, int64_t ldx, 
  * first ranked by the expansion ||c||^2 - 2 x.c (one FMA per dimension and
  * centroid) and a codebook whose two best centroids lie within that
  * computation's rounding bound is redone by direct differences, so the codes
- * equal BOLT_ENCODE_DIRECT's bit for bit.  BOLT_ENCODE_AUTO: EXPANDED for
- * j/m = 8 (measured faster on a B200), DIRECT otherwise.
+ * equal BOLT_ENCODE_DIRECT's bit for bit.  BOLT_ENCODE_AUTO: EXPANDED where
+ * it applies (measured faster on a B200), DIRECT otherwise.
  * Errors: as bolt_encode; RANGE for another variant. */
 enum { BOLT_ENCODE_AUTO = 0, BOLT_ENCODE_DIRECT = 1, BOLT_ENCODE_EXPANDED = 2 };
 BOLT_API bolt_status bolt_encode_ex(const float* X, int64_t n, int j, int64_t ldx, const float* C, int m,

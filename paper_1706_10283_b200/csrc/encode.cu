@@ -328,7 +328,7 @@ __device__ __noinline__ uint32_t direct_argmin_g(const float* __restrict__ x, co
     return arg;
 }
 
-template <int L, int NS, int RT, int W>
+template <int L, int NS, int RT, int W, int H>
 __global__ void __launch_bounds__(32 * W + 32, 1)
 encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ X, int64_t n, int64_t ldx,
                    const float* __restrict__ C, int m, uint32_t* __restrict__ codes, int64_t nblocks, int S,
@@ -345,9 +345,11 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
     constexpr int R = 32 * NS;           // rows per stage
     constexpr int SG = NS / RT;          // slab groups (of RT slabs)
     const int j = m * L;
-    const int nbox = j / 32;
-    const uint32_t stage_bytes = (uint32_t)R * j * 4;
-    const int cpw = m * SG / W;          // codebooks per compute warp (m * SG % W == 0)
+    const int jh = j / H;                // floats of a row per stage (H column parts per row block)
+    const int mh = m / H;                // codebooks per stage
+    const int nbox = jh / 32;
+    const uint32_t stage_bytes = (uint32_t)R * jh * 4;
+    const int cpw = mh * SG / W;         // codebooks per compute warp (mh * SG % W == 0)
     uint8_t* xs = enc_row_smem;                                          // [S][j/32][R][32] swizzled
     float* cm2 = reinterpret_cast<float*>(xs + (size_t)S * stage_bytes);  // [m][L][16] -2c
     float* cn = cm2 + (size_t)j * kK;                                    // [m][16]
@@ -387,8 +389,9 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
     if (warp == W) {
         // ------------------------------------------------ copy warp
         if (lane == 0) {
-            int i = 0;
-            for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
+            for (int i = 0;; ++i) {
+                const int64_t b = blockIdx.x + (int64_t)(i / H) * gridDim.x;  // row block, column part i % H
+                if (b >= nblocks) break;
                 const int s = i % S;
                 tc::mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(&full[s])),
@@ -399,24 +402,26 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
                     asm volatile(
                         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
                             "r"(dst + (uint32_t)bx * (R * 128)),
-                        "l"(&xmap), "r"(bx * 32), "r"((int)(b * R)), "r"(tc::smem_u32(&full[s]))
+                        "l"(&xmap), "r"((i % H) * jh + bx * 32), "r"((int)(b * R)), "r"(tc::smem_u32(&full[s]))
                         : "memory");
             }
         }
         return;
     }
     // ---------------------------------------------------- compute warps
-    int i = 0;
-    for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
+    for (int i = 0;; ++i) {
+        const int64_t b = blockIdx.x + (int64_t)(i / H) * gridDim.x;
+        if (b >= nblocks) break;
+        const int c0 = (i % H) * mh;  // first codebook of this stage
         const int s = i % S;
         const int64_t row_blk = b * R;
         uint32_t amb = 0;  // ambiguous (codebook, slab) items of this stage, bit cc RT + r
         tc::mbar_wait(&full[s], (i / S) & 1);
         const uint8_t* st = xs + (size_t)s * stage_bytes;
         for (int cc = 0; cc < (xm & 1 ? 0 : cpw); ++cc) {
-            const int c = (warp / SG) * cpw + cc;
+            const int c = c0 + (warp / SG) * cpw + cc;
             const int sl0 = (warp % SG) * RT;         // first slab of this warp
-            const int bx = (c * L) >> 5;              // box of this codebook's L floats
+            const int bx = ((c - c0) * L) >> 5;       // box of this codebook's L floats
             const int ch0 = ((c * L) & 31) >> 2;      // its first 16-byte chunk within the 128-byte row
             float xv[RT][L];
 #pragma unroll
@@ -521,7 +526,7 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
             const int bit = __ffs(amb) - 1;
             amb &= amb - 1;
             const int cc = bit / RT, r = bit - cc * RT;
-            const int c = (warp / SG) * cpw + cc;
+            const int c = c0 + (warp / SG) * cpw + cc;
             const int64_t row = row_blk + 32 * ((warp % SG) * RT + r) + lane;
             const uint32_t arg = direct_argmin_g<L>(X + row * ldx + c * L, C + (size_t)c * kK * L);
             const int pos = 4 * (int)(row & 7);
@@ -567,21 +572,25 @@ cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const f
     size_t smem = (size_t)j * kK * sizeof(float) + (size_t)kEncGroupsPerBlock * m * sizeof(uint32_t);
     bool vec = (L % 4 == 0) && (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
     int64_t blocks = ceil_div(n, kEncRowsPerBlock);
-    // AUTO: the expanded kernel for J/M = 8 (c2 0.185 vs 0.199 ms, c4 0.059 vs
-    // 0.067); J/M = 16 keeps the direct kernel (c3 0.70 vs 0.67 ms)
-    if ((mode == 2 || (mode == 0 && L == 8)) && (L == 8 || L == 16) && j % 32 == 0 && j <= 512 && m % 8 == 0 && (ldx % 4) == 0 &&
+    // AUTO: the expanded kernel where it applies (c2 0.184 vs 0.199 ms, c3
+    // 0.538 vs 0.671, c4 0.059 vs 0.067)
+    if ((mode == 2 || mode == 0) && (L == 8 || L == 16) && j % 32 == 0 && j <= 512 && m % 8 == 0 && (ldx % 4) == 0 &&
         (reinterpret_cast<uintptr_t>(X) & 15) == 0 && encode_tiled()) {
         // persistent whole-row TMA expanded-distance kernel (bit-identical codes)
-        const int NS = j <= 128 ? 4 : j <= 256 ? 2 : 1;  // 32-row slabs per stage (64 KB stages)
-        int W = 16, RT = NS == 1 ? 1 : 2;                // compute warps, slabs per thread
+        // H column parts per row block (J = 512: two stages of 64 rows x 256 floats),
+        // NS 32-row slabs per 64 KB stage, 16 compute warps of RT slabs each
+        const int H = j <= 256 ? 1 : 2;
+        const int jh = j / H;
+        const int NS = jh <= 128 ? 4 : 2;
+        int W = 16, RT = 2;
 #ifdef BOLT_XMODE
         if (getenv("BOLT_ENC_W8") && NS == 4) W = 8, RT = 4;
 #endif
         const int R = 32 * NS;
-        const size_t stage = (size_t)R * j * sizeof(float);
+        const size_t stage = (size_t)R * jh * sizeof(float);
         const size_t tables = (size_t)j * kK * sizeof(float) + (size_t)m * kK * sizeof(float) +
                               (size_t)((m + 1) & ~1) * sizeof(float);
-        const size_t budget = 227 * 1024 - 1024;
+        const size_t budget = 227 * 1024 - 256;
         int S = (int)std::min<size_t>(4, (budget - tables - 8 * sizeof(uint64_t)) / stage);
         int xm = 0;
 #ifdef BOLT_XMODE
@@ -593,18 +602,19 @@ cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const f
         const cuuint64_t strides[1] = {(cuuint64_t)(ldx * sizeof(float))};
         const cuuint32_t box[2] = {32u, (cuuint32_t)R};
         const cuuint32_t estr[2] = {1u, 1u};
-        if (S >= 2 && (m * (NS / RT)) % W == 0 &&
+        if (S >= 2 && ((m / H) * (NS / RT)) % W == 0 && n < (int64_t(1) << 31) &&
             encode_tiled()(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box,
                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
             const size_t tsmem = (size_t)S * stage + tables + 2 * (size_t)S * sizeof(uint64_t);
             const int64_t nblocks = ceil_div(n, (int64_t)R);
             const unsigned grid = (unsigned)std::min<int64_t>(nblocks, sms);
-            decltype(&encode_rows_kernel<8, 4, 2, 16>) kern;
-            if (L == 8) kern = NS == 4 ? (W == 8 ? encode_rows_kernel<8, 4, 4, 8> : encode_rows_kernel<8, 4, 2, 16>)
-                             : NS == 2 ? encode_rows_kernel<8, 2, 2, 16> : encode_rows_kernel<8, 1, 1, 16>;
-            else kern = NS == 4 ? encode_rows_kernel<16, 4, 2, 16>
-                        : NS == 2 ? encode_rows_kernel<16, 2, 2, 16> : encode_rows_kernel<16, 1, 1, 16>;
+            decltype(&encode_rows_kernel<8, 4, 2, 16, 1>) kern;
+            if (L == 8) kern = H == 2 ? encode_rows_kernel<8, 2, 2, 16, 2>
+                             : NS == 4 ? (W == 8 ? encode_rows_kernel<8, 4, 4, 8, 1> : encode_rows_kernel<8, 4, 2, 16, 1>)
+                                       : encode_rows_kernel<8, 2, 2, 16, 1>;
+            else kern = H == 2 ? encode_rows_kernel<16, 2, 2, 16, 2>
+                        : NS == 4 ? encode_rows_kernel<16, 4, 2, 16, 1> : encode_rows_kernel<16, 2, 2, 16, 1>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
             kern<<<grid, 32 * W + 32, tsmem, s>>>(xmap, X, n, ldx, C, m, codes, nblocks, S, xm);
             return cudaGetLastError();

@@ -80,18 +80,22 @@ def test_encode_centroid_identity(bolt, orc):
     np.testing.assert_array_equal(got, idx)
 
 
-@pytest.mark.parametrize("seed", [0, 1, 2])
-def test_encode_fast_equals_direct_near_ties(bolt, orc, seed):
+@pytest.mark.parametrize("seed,m,L", [(0, 16, 8), (1, 16, 8), (2, 16, 8),   # J = 128: 4 slabs per stage
+                                       (0, 32, 8),                           # J = 256 (c4): 2 slabs
+                                       (0, 32, 16), (1, 64, 8),              # J = 512 (c3): 2 column parts
+                                       (0, 8, 16)])                          # J/M = 16 in one 128-float part
+def test_encode_fast_equals_direct_near_ties(bolt, orc, seed, m, L):
     """The TMA-staged expanded-distance encoder (ENCODE_EXPANDED: ||c||^2 - 2 x.c ranking,
     rounding bound, direct fallback) returns the direct-difference kernel's
     codes bit for bit, on rows built at or near midpoints of centroid pairs
     (exact fp32 ties, 1e-5 .. 0.5 offsets) with c2-sized coordinates (0..255,
     where the expansion's rounding is largest), duplicated centroids and rows
     equal to centroids; and both agree with the oracle up to near-ties."""
-    m, L, n = 16, 8, 60_000
-    rng = np.random.default_rng(seed)
+    n = 60_000
+    rng = np.random.default_rng(seed + 100 * m + L)
     C = rng.uniform(0, 255, (m, 16, L)).astype(np.float32)
     C[:4, 9] = C[:4, 4]                       # exact duplicate centroids in 4 codebooks
+    C[m - 1, 15] = C[m - 1, 0]                # ... and in the last codebook (the last column part)
     a = rng.integers(0, 16, (n, m))
     b = rng.integers(0, 16, (n, m))
     mid = (C[np.arange(m)[None, :], a] + C[np.arange(m)[None, :], b]) / np.float32(2)
@@ -103,8 +107,8 @@ def test_encode_fast_equals_direct_near_ties(bolt, orc, seed):
     fast = host(bolt.encode(Xd, Cd, variant=bolt.ENCODE_EXPANDED))
     direct = host(bolt.encode(Xd, Cd, variant=bolt.ENCODE_DIRECT))
     np.testing.assert_array_equal(host(bolt.encode(Xd, Cd)), direct)
-    # ragged row counts (partial 512-row TMA blocks, partial groups)
-    for nn in (1, 7, 511, 513, 4099):
+    # ragged row counts (partial TMA row blocks, partial groups)
+    for nn in (1, 7, 63, 65, 511, 513, 4099):
         np.testing.assert_array_equal(host(bolt.encode(Xd[:nn], Cd, variant=bolt.ENCODE_EXPANDED)),
                                       host(bolt.encode(Xd[:nn], Cd, variant=bolt.ENCODE_DIRECT)))
     np.testing.assert_array_equal(fast, direct)
