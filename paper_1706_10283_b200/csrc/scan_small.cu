@@ -28,6 +28,9 @@ constexpr int kThreads = 256;  // 8 warps
 constexpr int kWarpsPB = kThreads / 32;
 constexpr int kBlocksPerSM = 2;
 constexpr int kMaxSlots = 32;  // minima slots per query (k <= 32)
+#ifndef BOLT_SMALL_EARLY
+#define BOLT_SMALL_EARLY 4  // sweep Q = 2, 4, 8: 0.508, 0.945, 1.752 -> 0.493, 0.920, 1.731 ms (every iteration: Q = 1 0.29 -> 0.44)
+#endif
 
 template <int QT, int M>
 __device__ __forceinline__ void load_group(const uint32_t* __restrict__ codes, int64_t g, bool valid,
@@ -183,7 +186,10 @@ topk_small_kernel(ScanArgs a, int k, int metric, int64_t index_base, int tiles, 
         for (int i = 0; i < M / 4; ++i) w[i] = wnext[i];
         load_group<QT, M>(a.codes, g + 32, g + 32 < gend, wnext);
         const int nrows = g < gend ? (int)min64(8, a.n - g * 8) : 0;
-        const bool refresh = ((gs - gbeg) & (32 * 8 - 1)) == 0;  // shared bounds re-read every 8 iterations
+        // shared bounds re-read every iteration while they are still loose (the
+        // first BOLT_SMALL_EARLY iterations of a warp), then every 8
+        const int64_t it = (gs - gbeg) >> 5;
+        const bool refresh = it < BOLT_SMALL_EARLY || (it & 7) == 0;
 #pragma unroll 1
         for (int q = 0; q < QT; ++q) {
             if (q0 + q >= a.nq) break;
