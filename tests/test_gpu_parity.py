@@ -377,6 +377,23 @@ def test_topk_constant_tables_all_ties(bolt, orc):
         np.testing.assert_array_equal(host(idx)[0], np.arange(k))
 
 
+@pytest.mark.parametrize("w,nq,k", [(1, 3, 10), (5, 7, 10), (36, 50, 10), (40, 3, 128), (160, 20, 10),
+                                     (256, 4, 12), (257, 4, 5), (300, 2, 32)])
+def test_merge_matches_sorted_union(bolt, w, nq, k):
+    """bolt_topk_merge = the k smallest keys of the union of the w sorted lists
+    (warp-per-query kernel for w <= 256, block tournament above), with padded
+    list tails, a fully padded list and a query whose lists are all padding."""
+    r = np.random.default_rng([7, w, nq, k])
+    keys = np.sort(r.integers(0, 2**62, (w, nq, k), dtype=np.int64), axis=2).view(np.uint64)
+    mx = np.iinfo(np.uint64).max
+    keys[0, :, k // 2:] = mx
+    keys[w - 1, 0, :] = mx
+    keys[:, nq - 1, :] = mx if nq > 1 else keys[:, nq - 1, :]
+    got = host(bolt.topk_merge(dev(keys)))
+    exp = np.sort(keys.transpose(1, 0, 2).reshape(nq, -1), axis=1)[:, :k]
+    np.testing.assert_array_equal(got, exp)
+
+
 def test_merge_and_split(bolt, orc):
     n, m, nq, k = 6000, 8, 12, 20
     flat = G.random_codes(n, m, 21)
