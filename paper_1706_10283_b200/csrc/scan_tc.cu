@@ -402,7 +402,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, uint64_t* __restrict__ part_keys,
                uint32_t* __restrict__ gthr_inv, int xmode, FullOut fo, const __grid_constant__ CUtensorMap omap) {
 #ifndef BOLT_XMODE
+#ifdef BOLT_XCONST
+    xmode = BOLT_XCONST;  // diagnostic builds with one stage switch compiled in as a constant (tools/)
+#else
     xmode = 0;  // diagnostic stage switches exist only in libbolt_x.so (tools/)
+#endif
 #endif
     using C = Cfg<M, (kOut == 1 || kOut == 2), (kOut == 3 ? kNQ / 2 : kQM),
                   (kOut == 3 ? kEpiWarps * (kNQ / 2) * 32 * 4 : 0), kPairT>;
