@@ -95,6 +95,12 @@ constexpr int kMmaWarp = kProdWarps + kEpiWarps;
 // stages gate the MMA, win issue slots over the epilogue's filter work.
 constexpr int kThreads = (kMmaWarp + 1) * 32;
 constexpr int kPrefetch = 3;             // tiles of code words in flight per producer thread
+#ifndef BOLT_TC_KMAX10
+#define BOLT_TC_KMAX10 1  // k <= 10: 10-slot register lists (c2 scan 1.705 -> 1.687 ms)
+#endif
+#ifndef BOLT_TC_MINMAX_INSERT
+#define BOLT_TC_MINMAX_INSERT 1  // min/max bubble insert (c2 scan 1.687 -> 1.678 ms)
+#endif
 // u32 words of shared scratch per epilogue thread: top-k parks 32 u16 values
 // (80-byte rows: 16-byte aligned, conflict-free); full output stages a 32-row x
 // 128-byte block per warp (4 KB)
@@ -166,12 +172,20 @@ struct RegList {
     // left neighbour (depth 3, instead of a KMAX-long min/max chain: the
     // slow path is latency-bound).
     __device__ __forceinline__ void insert(uint32_t c) {
+#if BOLT_TC_MINMAX_INSERT
+        // v'[i] = max(v[i-1], min(v[i], c)): each slot from the old values
+        // only (depth 2, one min and one max per slot)
+#pragma unroll
+        for (int i = KMAX - 1; i > 0; --i) v[i] = max(v[i - 1], min(v[i], c));
+        v[0] = min(v[0], c);
+#else
         bool lt[KMAX];
 #pragma unroll
         for (int i = 0; i < KMAX; ++i) lt[i] = v[i] < c;
 #pragma unroll
         for (int i = KMAX - 1; i > 0; --i) v[i] = lt[i] ? v[i] : (lt[i - 1] ? c : v[i - 1]);
         v[0] = lt[0] ? v[0] : c;
+#endif
     }
     __device__ __forceinline__ uint32_t threshold(int idx_bits) const {
         return v[KMAX - 1] == 0xFFFFFFFFu ? kNotFull : (v[KMAX - 1] >> idx_bits);
@@ -1085,10 +1099,15 @@ template <int M, bool kPairT>
 cudaError_t launch_mp(const ScanArgs& a, int k, int metric, int64_t index_base, int rparts, uint64_t* part_keys,
                       uint32_t* gthr, cudaStream_t s) {
     const bool dot = metric == BOLT_DOT;
-    // register list capacity: smallest of {4, 12, 16, 32} >= k (bubble cost ~ 2 KMAX)
+    // register list capacity: smallest of {4, 10, 12, 16, 32} >= k (bubble cost ~ 3 KMAX)
     if (k <= 4)
         return dot ? launch_mk<M, true, 4, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s)
                    : launch_mk<M, false, 4, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s);
+#if BOLT_TC_KMAX10
+    if (k <= 10)
+        return dot ? launch_mk<M, true, 10, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s)
+                   : launch_mk<M, false, 10, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s);
+#endif
     if (k <= 12)
         return dot ? launch_mk<M, true, 12, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s)
                    : launch_mk<M, false, 12, 0, false, 0, kPairT>(a, k, index_base, rparts, part_keys, gthr, s);
