@@ -12,6 +12,10 @@
 // tables exact away from rounding boundaries.
 #include "common.cuh"
 
+#ifndef BOLT_LUT_QC
+#define BOLT_LUT_QC 1  // 0: one thread per entry (A/B builds)
+#endif
+
 namespace bolt {
 namespace {
 
@@ -53,6 +57,49 @@ __global__ void build_luts_kernel(const float* __restrict__ Q, int64_t nq, int j
     }
 }
 
+// One thread per (query, codebook), the 16 entries of its table in
+// registers: lane = query (32 consecutive queries per warp), warp-uniform
+// codebook, so the centroid loads are broadcasts; the same fp64 operations
+// in the same order as build_luts_kernel (bit-identical), the 16 quantized
+// entries written as one 16-byte store.
+template <int L>
+__global__ void __launch_bounds__(256)
+build_luts_qc_kernel(const float* __restrict__ Q, int64_t nq, int64_t ldq, const float* __restrict__ C, int m,
+                     int metric, double a, const float* __restrict__ b, uint8_t* __restrict__ qluts,
+                     float* __restrict__ luts32, double* __restrict__ luts64) {
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // global warp
+    const int lane = threadIdx.x & 31;
+    const int c = (int)(wg % m);
+    const int64_t q = (wg / m) * 32 + lane;
+    if (q >= nq) return;
+    double x[L];
+    const float* qv = Q + q * ldq + (int64_t)c * L;
+#pragma unroll
+    for (int d = 0; d < L; ++d) x[d] = (double)__ldg(qv + d);
+    const double bc = qluts ? (double)__ldg(b + c) : 0.0;  // b is only given for quantized tables
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int i = 0; i < kK; ++i) {
+        const float* cv = C + ((int64_t)c * kK + i) * L;
+        double y = 0.0;
+        if (metric == BOLT_L2SQ) {
+#pragma unroll
+            for (int d = 0; d < L; ++d) {
+                const double diff = __dsub_rn(x[d], (double)__ldg(cv + d));
+                y = __dadd_rn(y, __dmul_rn(diff, diff));
+            }
+        } else {
+#pragma unroll
+            for (int d = 0; d < L; ++d) y = __dadd_rn(y, __dmul_rn(x[d], (double)__ldg(cv + d)));
+        }
+        const int64_t e = (q * m + c) * kK + i;
+        if (luts64) luts64[e] = y;
+        if (luts32) luts32[e] = (float)y;
+        w[i >> 2] |= (uint32_t)quantize_one(y, a, bc) << (8 * (i & 3));
+    }
+    if (qluts) *reinterpret_cast<uint4*>(qluts + (q * m + c) * kK) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 __global__ void quantize_kernel(const float* __restrict__ luts, int64_t nq, int m, double a,
                                 const float* __restrict__ b, uint8_t* __restrict__ qluts) {
     const int64_t total = nq * m * kK;
@@ -75,6 +122,15 @@ cudaError_t launch_build_luts(const float* Q, int64_t nq, int j, int64_t ldq, co
                               double* luts64, cudaStream_t s) {
     const int64_t total = nq * m * kK;
     if (total == 0) return cudaSuccess;
+    const int L = j / m;
+    const bool q16 = qluts == nullptr || (reinterpret_cast<uintptr_t>(qluts) & 15) == 0;
+    if (BOLT_LUT_QC && q16 && (L == 4 || L == 8 || L == 16)) {
+        const int64_t threads = ceil_div(nq, (int64_t)32) * 32 * m;  // warps of 32 queries x codebooks
+        const unsigned blocks = (unsigned)ceil_div(threads, (int64_t)256);
+        auto kern = L == 4 ? build_luts_qc_kernel<4> : L == 8 ? build_luts_qc_kernel<8> : build_luts_qc_kernel<16>;
+        kern<<<blocks, 256, 0, s>>>(Q, nq, ldq, C, m, metric, (double)a, b, qluts, luts32, luts64);
+        return cudaGetLastError();
+    }
     build_luts_kernel<<<grid_for(total, 256), 256, 0, s>>>(Q, nq, j, ldq, C, m, metric, (double)a, b,
                                                          qluts, luts32, luts64);
     return cudaGetLastError();
