@@ -227,7 +227,7 @@ BOLT_API bolt_status bolt_keys_split(const uint64_t* keys, int64_t count, bolt_m
 /* ------------------------------------------- Bolt No Quantize (fp32 tables) */
 /* The variant of P:L390 that skips table quantization: the
  * running total of P:L224-231 over the fp32 tables D of bolt_build_luts,
- * summed in fp32 in ascending codebook order from 0 (R17).
+ * summed in fp32 in ascending codebook order from 0 (R18).
  *   luts [nq][m][16] fp32 (4 B aligned); codes layout v1 for n rows (16 B aligned)
  *   out  fp32, out[i*ldo + q], ldo >= nq
  * Errors: NULL, SHAPE (m not in 1..64, n or nq < 0, ldo < nq), ALIGN. */

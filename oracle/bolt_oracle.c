@@ -360,7 +360,7 @@ void oracle_topk(const uint8_t* codes, int64_t n, int M, const uint8_t* qluts, i
 
 /* --------------------------------------------------------------- O13 -- */
 /* "Bolt No Quantize": the scan with the unquantized
- * tables, out[i*nq + q] = sum_m D[q][m][i_m] with D the fp32 tables.  R17:
+ * tables, out[i*nq + q] = sum_m D[q][m][i_m] with D the fp32 tables.  R18:
  * summed in fp32, in ascending m from 0.0f -- the paper fixes no precision for
  * this variant, so the oracle takes the kernel's, and a top-k decided by these
  * sums is then exact (the near-tie rule of the parity contract). */

@@ -184,7 +184,7 @@ def topk(codes, qluts, k: int, metric: int, index_base: int = 0):
 
 def scan_f32(codes, luts32):
     """O13 (Bolt No Quantize): flat codes u8 [n][M], fp32 tables [nq][M][16] ->
-    fp32 [n][nq], summed in fp32 in ascending m (R17)."""
+    fp32 [n][nq], summed in fp32 in ascending m (R18)."""
     codes = np.ascontiguousarray(codes, dtype=np.uint8)
     luts32 = np.ascontiguousarray(luts32, dtype=np.float32)
     n, M = codes.shape

@@ -4,7 +4,7 @@
 // The paper keeps this variant only to show that table quantization costs no
 // accuracy ("it sacrifices Bolt's high speed"); here it is the same layout-v1
 // codes read against fp32 tables held in shared memory.  Sums run in fp32 in
-// ascending m from 0.0f (R17), so a top-k decided by them is exact against the
+// ascending m from 0.0f (R18), so a top-k decided by them is exact against the
 // oracle given the same fp32 tables.  Lookups are LDS from a 16-word table:
 // the 32 lanes of a warp (32 rows) read one (query, codebook) table, whose 16
 // entries lie in 16 distinct banks -- conflict-free whatever the codes.
