@@ -98,6 +98,9 @@ constexpr int kPrefetch = 3;             // tiles of code words in flight per pr
 #ifndef BOLT_TC_KMAX10
 #define BOLT_TC_KMAX10 1  // k <= 10: 10-slot register lists (c2 scan 1.705 -> 1.687 ms)
 #endif
+#ifndef BOLT_TC_ONECAND
+#define BOLT_TC_ONECAND 1  // slow path: a lone candidate taken from the chunk minimum, no scratch round trip (c2 scan 1.679 -> 1.633 ms)
+#endif
 #ifndef BOLT_TC_MINMAX_INSERT
 #define BOLT_TC_MINMAX_INSERT 1  // min/max bubble insert (c2 scan 1.687 -> 1.678 ms)
 #endif
@@ -902,6 +905,25 @@ topk_tc_kernel(ScanArgs a, int k, int64_t index_base, int64_t vpp, int tiles_q, 
                     // this thread's scratch row, per-lane loop over its candidates
                     uint32_t mask = thr == kNotFull ? 0xFFFFFFFFu
                                                     : candidate_mask<kDot>(p[c], (kDot ? C::KVMAX - thr : thr) * 0x10001u);
+#if BOLT_TC_ONECAND
+                    // one candidate: it is the chunk's best value (every other
+                    // value is at or above thr), so no scratch round trip
+                    if ((mask & (mask - 1)) == 0) {
+                        if (mask) {
+                            const int bpos = __ffs(mask) - 1;
+                            const int j = 4 * (bpos & 7) + (bpos >> 3);
+                            const uint32_t kv = kDot ? C::KVMAX - cbest : cbest;
+                            const uint32_t key = (kv << C::IDX_BITS) | (uint32_t)(tbl + col + j);
+                            if (key < list.v[KMAX - 1] && j < nleft) {
+                                list.insert(key);
+                                own = list.threshold(C::IDX_BITS);
+                                thr = min(thr, own);
+                                changed = true;
+                            }
+                        }
+                        continue;
+                    }
+#endif
                     uint4* sv = reinterpret_cast<uint4*>(scratch);
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
