@@ -273,6 +273,25 @@ __device__ __noinline__ uint32_t direct_argmin(const float* __restrict__ x, cons
     return arg;
 }
 
+// A/B switch (tools/): 0 rebuilds the round-2 epilogue (two LOP3 per tag,
+// 64-bit row arithmetic per stored word)
+#ifndef BOLT_ENC_LEAN
+#define BOLT_ENC_LEAN 2
+#endif
+#ifndef BOLT_ENC_FB_SMEM
+#define BOLT_ENC_FB_SMEM 1
+#endif
+
+// (x & mask) | K in one LOP3: with the mask in a register and the 4-bit
+// centroid index as the immediate (ptxas splits the all-immediate form into
+// an AND and an OR)
+template <uint32_t K>
+__device__ __forceinline__ float tag_low4(float x, uint32_t mask) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(__float_as_uint(x)), "r"(mask), "n"(K));
+    return __uint_as_float(d);
+}
+
 // Expanded distances (BOLT_ENCODE_EXPANDED): per
 // centroid s_k = fl(||c_k||^2) + sum_t x_t (-2 c_kt) as one packed FFMA chain
 // (one FFMA per (dimension, centroid) instead of a subtract and an FFMA),
@@ -284,8 +303,10 @@ __device__ __noinline__ uint32_t direct_argmin(const float* __restrict__ x, cons
 //
 // Bound (u = 2^-24, g(n) = n u / (1 - n u)): the FFMA chain of L terms from
 // n_k = fl(||c_k||^2) errs by <= g(L)(|n_k| + 2 sum_t |x_t||c_kt|), n_k by
-// <= g(L)||c_k||^2, so |s^_k - s_k| <= E = 4 g(L)(C2 + 2 AX) with C2 >= max_k
-// n_k and AX = sum_t |x_t| max_k |c_kt|.  The direct fp32 distance errs by
+// <= g(L)||c_k||^2; with 2 sum_t |x_t||c_kt| <= ||x||^2 + ||c_k||^2 that is
+// |s^_k - s_k| < 1.5 g(L)(1 + g(L)) A, A = 2 C2 + X2 (C2 >= max_k n_k, X2 >=
+// ||x||^2 of the slice), and E = 2 g(L) A bounds it (round 2's first
+// version: 4 g(L) A, twice the fallbacks).  The direct fp32 distance errs by
 // <= g(L+2) d_k.  With b1 = min_k s^_k and every other s^_k >= b1 + need,
 // need = 2.5 E + 3 g(L+2)(X2 + |b1| + E) (X2 >= ||x||^2), the direct
 // distances keep the same unique minimum.  The factors carry a >= 25 % slack
@@ -328,6 +349,48 @@ __device__ __noinline__ uint32_t direct_argmin_g(const float* __restrict__ x, co
     return arg;
 }
 
+// direct_argmin from shared memory: x from the stage's swizzled row (rowp, the
+// slice's first 16-byte chunk ch0, row rl) and the centroids from the -2c
+// table, -c = 0.5 * (-2c) exactly, so fma(-2c, 0.5, x) is the direct kernel's
+// fl(x + (-c)) and the distances are its fp32 operations in its order.  The
+// expanded kernel's fallback (A/B: BOLT_ENC_FB_SMEM=0 reads X and C from
+// global memory, round 2's first version).
+template <int L>
+__device__ __noinline__ uint32_t direct_argmin_s(const uint8_t* __restrict__ rowp, int ch0, int rl,
+                                                 const float* __restrict__ ccm) {
+    float xv[L];
+#pragma unroll
+    for (int h = 0; h < L / 4; ++h) {
+        const float4 v = *reinterpret_cast<const float4*>(rowp + (((ch0 + h) ^ (rl & 7)) << 4));
+        xv[4 * h] = v.x; xv[4 * h + 1] = v.y; xv[4 * h + 2] = v.z; xv[4 * h + 3] = v.w;
+    }
+    float2 d[kK / 2];
+#pragma unroll
+    for (int p = 0; p < kK / 2; ++p) d[p] = make_float2(0.f, 0.f);
+    const float2 hf = make_float2(0.5f, 0.5f);
+#pragma unroll
+    for (int t = 0; t < L; ++t) {
+        const float2 xx = make_float2(xv[t], xv[t]);
+        const float4* cv = reinterpret_cast<const float4*>(ccm + (size_t)t * kK);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float4 c4 = cv[q];
+            const float2 da = __ffma2_rn(make_float2(c4.x, c4.y), hf, xx);
+            const float2 db = __ffma2_rn(make_float2(c4.z, c4.w), hf, xx);
+            d[2 * q] = __ffma2_rn(da, da, d[2 * q]);
+            d[2 * q + 1] = __ffma2_rn(db, db, d[2 * q + 1]);
+        }
+    }
+    float best = d[0].x;
+    uint32_t arg = 0;
+#pragma unroll
+    for (int p = 0; p < kK / 2; ++p) {
+        if (p > 0 && d[p].x < best) { best = d[p].x; arg = 2 * p; }
+        if (d[p].y < best) { best = d[p].y; arg = 2 * p + 1; }
+    }
+    return arg;
+}
+
 template <int L, int NS, int RT, int W, int H>
 __global__ void __launch_bounds__(32 * W + 32, 1)
 encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ X, int64_t n, int64_t ldx,
@@ -341,6 +404,17 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
     constexpr float kU = 5.9604645e-8f;  // 2^-24
     constexpr float kGL = (float)L * kU / (1.0f - (float)L * kU);
     constexpr float kGL2 = (float)(L + 2) * kU / (1.0f - (float)(L + 2) * kU);
+    // E = kE g(L) A: the chain errs by <= g(L)(|n_k| + 2 sum|x_t||c_kt|) <= g(L)(1 + g(L))(2 C2 + X2)
+    // and n_k by <= g(L) C2, together < 1.5 g(L)(1 + g(L)) A; kE = 2 keeps > 25 % slack
+    // (BOLT_ENC_E4: round 2's first factor, 4)
+#ifdef BOLT_ENC_E4
+    constexpr float kE = 4.0f;
+#else
+    constexpr float kE = 2.0f;
+#endif
+    constexpr float kN1 = 2.5f * kE * kGL + 3.0f * kGL2 * kE * kGL;
+    constexpr float kN3 = (kN1 + 3.0f * kGL2) * (1.0f + 2.0f * kGL);   // on the computed ||x||^2 (rounded up by 1 + 2 g(L))
+    constexpr float kN4 = 3.0f * kGL2;
     static_assert(NS % RT == 0, "slab groups");
     constexpr int R = 32 * NS;           // rows per stage
     constexpr int SG = NS / RT;          // slab groups (of RT slabs)
@@ -354,7 +428,8 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
     float* cm2 = reinterpret_cast<float*>(xs + (size_t)S * stage_bytes);  // [m][L][16] -2c
     float* cn = cm2 + (size_t)j * kK;                                    // [m][16]
     float* c2max = cn + (size_t)m * kK;                                  // [m]
-    uint64_t* full = reinterpret_cast<uint64_t*>(c2max + ((m + 1) & ~1));
+    uint32_t* tagmask = reinterpret_cast<uint32_t*>(c2max + ((m + 1) & ~1));  // [2]: ~0xF, kept out of ptxas's sight
+    uint64_t* full = reinterpret_cast<uint64_t*>(tagmask + 2);
     uint64_t* empty = full + S;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -383,8 +458,15 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
     for (int c = tid; c < m; c += blockDim.x) {
         float a = 0.f;
         for (int k = 0; k < kK; ++k) a = fmaxf(a, fabsf(cn[c * kK + k]));
+#if BOLT_ENC_LEAN == 2
+        // need = 2.5 E + 3 g(L+2)(X2 + |b1| + E) with E = kE g(L)(2 C2 + X2), sorted by
+        // variable: kN1 2 C2 (this table) + kN3 ||x||^2 + kN4 |b1|
+        c2max[c] = 2.0f * kN1 * (a * (1.0f + 2.0f * kGL));
+#else
         c2max[c] = a * (1.0f + 2.0f * kGL);
+#endif
     }
+    if (tid == 0) tagmask[0] = ~0xFu;
     __syncthreads();
     if (warp == W) {
         // ------------------------------------------------ copy warp
@@ -416,6 +498,14 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
         const int s = i % S;
         const int64_t row_blk = b * R;
         uint32_t amb = 0;  // ambiguous (codebook, slab) items of this stage, bit cc RT + r
+#if BOLT_ENC_LEAN
+        // 32-bit row arithmetic within the stage: rows left in it, its first code word
+        const int nrem = (int)min64(n - row_blk, (int64_t)R);
+        uint32_t* const cst = codes + (row_blk >> 3) * m;
+        const uint32_t tmask = tagmask[0];
+        // this lane's group word of the warp's first slab (slab r: + 4 r m words)
+        uint32_t* const wp = cst + ((32 * ((warp % SG) * RT) + lane) >> 3) * m;
+#endif
         tc::mbar_wait(&full[s], (i / S) & 1);
         const uint8_t* st = xs + (size_t)s * stage_bytes;
         for (int cc = 0; cc < (xm & 1 ? 0 : cpw); ++cc) {
@@ -476,12 +566,62 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
             const float c2 = c2max[c];
 #pragma unroll
             for (int r = 0; r < RT; ++r) {
+#if BOLT_ENC_LEAN
+                const int lrow = 32 * (sl0 + r) + lane;
+                const bool valid = lrow < nrem;
+#else
                 const int64_t row = row_blk + 32 * (sl0 + r) + lane;
                 const bool valid = row < n;
+#endif
+#if BOLT_ENC_LEAN == 2
+                // Bit-group minima (no index tags): m[j][b] = min of the values whose
+                // index has bit j = b.  The minimum is min(m[j][0], m[j][1]) for any j;
+                // the runner-up differs from the argmin in some bit j, where it is the
+                // other group's minimum, and every max(m[j][0], m[j][1]) is the minimum
+                // of a group without the argmin, so second = min_j max(m[j][0], m[j][1]);
+                // bit j of the argmin is m[j][1] < m[j][0] (an exact tie makes
+                // second == min: ambiguous, redone by direct differences).
+                static_assert(kK == 16, "four index bits");
+                float pm[8], qm[4];
+#pragma unroll
+                for (int p = 0; p < 8; ++p) pm[p] = fminf(sv[r][p].x, sv[r][p].y);
+#pragma unroll
+                for (int p = 0; p < 4; ++p) qm[p] = fminf(pm[2 * p], pm[2 * p + 1]);
+                const float m30 = fminf(qm[0], qm[1]), m31 = fminf(qm[2], qm[3]);
+                const float m20 = fminf(qm[0], qm[2]), m21 = fminf(qm[1], qm[3]);
+                const float m10 = fminf(fminf(pm[0], pm[2]), fminf(pm[4], pm[6]));
+                const float m11 = fminf(fminf(pm[1], pm[3]), fminf(pm[5], pm[7]));
+                const float m00 = fminf(fminf(fminf(sv[r][0].x, sv[r][1].x), sv[r][2].x),
+                                        fminf(fminf(fminf(sv[r][3].x, sv[r][4].x), sv[r][5].x),
+                                              fminf(sv[r][6].x, sv[r][7].x)));
+                const float m01 = fminf(fminf(fminf(sv[r][0].y, sv[r][1].y), sv[r][2].y),
+                                        fminf(fminf(fminf(sv[r][3].y, sv[r][4].y), sv[r][5].y),
+                                              fminf(sv[r][6].y, sv[r][7].y)));
+                const float b1 = fminf(m30, m31);
+                const float b2 = fminf(fminf(fminf(fmaxf(m00, m01), fmaxf(m10, m11)), fmaxf(m20, m21)), fmaxf(m30, m31));
+                // sign bits of m[j][1] - m[j][0], funnel-shifted together (bit 3 first)
+                uint32_t argb = __float_as_uint(m31 - m30) >> 31;
+                argb = __funnelshift_l(__float_as_uint(m21 - m20), argb, 1);
+                argb = __funnelshift_l(__float_as_uint(m11 - m10), argb, 1);
+                argb = __funnelshift_l(__float_as_uint(m01 - m00), argb, 1);
+#else
                 // index k in the low 4 mantissa bits of s^_k (a change of < 2^-19 |s^_k|):
                 // the minimum of the tagged values names its centroid; a (min,
                 // second) tree gives the two smallest
                 float lo[kK / 2], hi[kK / 2];
+#if BOLT_ENC_LEAN
+#define BOLT_TAG_PAIR(P)                                                   \
+    {                                                                      \
+        const float e0 = tag_low4<2u * (P)>(sv[r][P].x, tmask);            \
+        const float e1 = tag_low4<2u * (P) + 1u>(sv[r][P].y, tmask);       \
+        lo[P] = fminf(e0, e1);                                             \
+        hi[P] = fmaxf(e0, e1);                                             \
+    }
+                BOLT_TAG_PAIR(0) BOLT_TAG_PAIR(1) BOLT_TAG_PAIR(2) BOLT_TAG_PAIR(3)
+                BOLT_TAG_PAIR(4) BOLT_TAG_PAIR(5) BOLT_TAG_PAIR(6) BOLT_TAG_PAIR(7)
+#undef BOLT_TAG_PAIR
+                static_assert(kK == 16, "eight tagged pairs");
+#else
 #pragma unroll
                 for (int p = 0; p < kK / 2; ++p) {
                     const float e0 = __uint_as_float((__float_as_uint(sv[r][p].x) & ~0xFu) | (2u * p));
@@ -489,6 +629,7 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
                     lo[p] = fminf(e0, e1);
                     hi[p] = fmaxf(e0, e1);
                 }
+#endif
 #pragma unroll
                 for (int w = kK / 4; w >= 1; w /= 2)
 #pragma unroll
@@ -498,23 +639,37 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
                         lo[p] = l;
                     }
                 const float b1 = lo[0], b2 = hi[0];
+#endif
                 // |s^_k| <= A = 2 C2 + X2 (2|x.c| <= X2 + ||c||^2), so E = 4 g(L) A
                 // bounds |s^_k - s_k| (2 sum|x_t||c_kt| <= X2 + C2) and the tags move
                 // each value by < 2^-19 A; need' = need + 2 * 2^-19 A (25 % slack)
+#if BOLT_ENC_LEAN == 2
+                // the same need without the tag term (no tags), as two FFMAs on the
+                // per-codebook constant
+                const float need = __fmaf_rn(kN4, fabsf(b1), __fmaf_rn(kN3, x2p[r].x + x2p[r].y, c2));
+                const bool ambig = !(b2 >= b1 + need) && valid;
+                const uint32_t arg = valid ? argb : 0u;
+#else
                 const float X2 = (x2p[r].x + x2p[r].y) * (1.0f + 2.0f * kGL);
                 const float A = 2.0f * c2 + X2;
                 const float E = 4.0f * kGL * A;
                 const float need = 2.5f * E + 3.0f * kGL2 * (X2 + fabsf(b1) + E) + 1.25f * 3.8146973e-6f * A;
                 const bool ambig = !(b2 >= b1 + need) && valid;
                 const uint32_t arg = valid ? (__float_as_uint(b1) & 0xFu) : 0u;
+#endif
                 amb |= (ambig ? 1u : 0u) << (cc * RT + r);
                 // layout-v1 word of this row's group: 8 consecutive lanes hold its 8 rows
                 uint32_t v = arg << (4 * (lane & 7));
                 v |= __shfl_xor_sync(0xffffffffu, v, 1);
                 v |= __shfl_xor_sync(0xffffffffu, v, 2);
                 v |= __shfl_xor_sync(0xffffffffu, v, 4);
+#if BOLT_ENC_LEAN
+                // the group's first row is this lane's: it exists iff the row does
+                if ((lane & 7) == 0 && valid && !(xm & 4)) wp[4 * r * m + c] = v;
+#else
                 const int64_t g = row >> 3;
                 if ((lane & 7) == 0 && g * kRowsPerWord < n && !(xm & 4)) codes[g * m + c] = v;
+#endif
             }
         }
         // ambiguous (row, codebook) slices: direct differences (the direct
@@ -528,7 +683,13 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
             const int cc = bit / RT, r = bit - cc * RT;
             const int c = c0 + (warp / SG) * cpw + cc;
             const int64_t row = row_blk + 32 * ((warp % SG) * RT + r) + lane;
+#if BOLT_ENC_FB_SMEM
+            const int rl = 32 * ((warp % SG) * RT + r) + lane;
+            const uint32_t arg = direct_argmin_s<L>(st + (size_t)(((c - c0) * L) >> 5) * (R * 128) + rl * 128,
+                                                    ((c * L) & 31) >> 2, rl, cm2 + (size_t)c * L * kK);
+#else
             const uint32_t arg = direct_argmin_g<L>(X + row * ldx + c * L, C + (size_t)c * kK * L);
+#endif
             const int pos = 4 * (int)(row & 7);
             uint32_t* w = codes + (row >> 3) * m + c;
             atomicAnd(w, ~(0xFu << pos));
@@ -589,7 +750,7 @@ cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const f
         const int R = 32 * NS;
         const size_t stage = (size_t)R * jh * sizeof(float);
         const size_t tables = (size_t)j * kK * sizeof(float) + (size_t)m * kK * sizeof(float) +
-                              (size_t)((m + 1) & ~1) * sizeof(float);
+                              (size_t)(((m + 1) & ~1) + 2) * sizeof(float);  // + the tag mask word
         const size_t budget = 227 * 1024 - 256;
         int S = (int)std::min<size_t>(4, (budget - tables - 8 * sizeof(uint64_t)) / stage);
         int xm = 0;
