@@ -32,6 +32,10 @@ constexpr int kMaxSlots = 32;  // minima slots per query (k <= 32)
 #define BOLT_SMALL_EARLY 4  // sweep Q = 2, 4, 8: 0.508, 0.945, 1.752 -> 0.493, 0.920, 1.731 ms (every iteration: Q = 1 0.29 -> 0.44)
 #endif
 
+#ifndef BOLT_SMALL_IADD3
+#define BOLT_SMALL_IADD3 0
+#endif
+
 template <int QT, int M>
 __device__ __forceinline__ void load_group(const uint32_t* __restrict__ codes, int64_t g, bool valid,
                                            uint4 (&w)[M / 4]) {
@@ -74,10 +78,19 @@ __device__ __forceinline__ void group_sums(const uint4 (&w)[M / 4], const uint4*
             for (int q = 0; q < QT; ++q) {
                 const uint4 lo = tab[2 * (q * M + t)];
                 const uint4 hi = tab[2 * (q * M + t) + 1];
+#if BOLT_SMALL_IADD3
+                // A/B: the two halves' lookups added by one 3-input ALU add each
+                // (4 IADD3 instead of 8 FMA-pipe IMADs per code word)
+                aL0[q] = aL0[q] + prmt(lo.x, lo.y, s0) + prmt(lo.z, lo.w, x0);
+                aH0[q] = aH0[q] + prmt(hi.x, hi.y, s0) + prmt(hi.z, hi.w, x0);
+                aL1[q] = aL1[q] + prmt(lo.x, lo.y, s1) + prmt(lo.z, lo.w, x1);
+                aH1[q] = aH1[q] + prmt(hi.x, hi.y, s1) + prmt(hi.z, hi.w, x1);
+#else
                 aL0[q] = imad(prmt(lo.z, lo.w, x0), one, imad(prmt(lo.x, lo.y, s0), one, aL0[q]));
                 aH0[q] = imad(prmt(hi.z, hi.w, x0), one, imad(prmt(hi.x, hi.y, s0), one, aH0[q]));
                 aL1[q] = imad(prmt(lo.z, lo.w, x1), one, imad(prmt(lo.x, lo.y, s1), one, aL1[q]));
                 aH1[q] = imad(prmt(hi.z, hi.w, x1), one, imad(prmt(hi.x, hi.y, s1), one, aH1[q]));
+#endif
             }
         }
 #pragma unroll
