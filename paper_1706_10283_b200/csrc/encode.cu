@@ -458,7 +458,7 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
     for (int c = tid; c < m; c += blockDim.x) {
         float a = 0.f;
         for (int k = 0; k < kK; ++k) a = fmaxf(a, fabsf(cn[c * kK + k]));
-#if BOLT_ENC_LEAN == 2
+#if BOLT_ENC_LEAN >= 2
         // need = 2.5 E + 3 g(L+2)(X2 + |b1| + E) with E = kE g(L)(2 C2 + X2), sorted by
         // variable: kN1 2 C2 (this table) + kN3 ||x||^2 + kN4 |b1|
         c2max[c] = 2.0f * kN1 * (a * (1.0f + 2.0f * kGL));
@@ -573,7 +573,41 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
                 const int64_t row = row_blk + 32 * (sl0 + r) + lane;
                 const bool valid = row < n;
 #endif
-#if BOLT_ENC_LEAN == 2
+#if BOLT_ENC_LEAN == 3
+                // A/B: runner-up test and argmin on the FMA pipe.  b1 = min (3-input
+                // tree), y_k = s^_k - b1 >= 0, z_k = sat(y_k / need) in [0, 1]: z = 0 for
+                // the argmin and 1 for every value at least need above it, so the slice
+                // is unambiguous iff sum z_k = 15, and then sum k z_k = 120 - argmin.
+                // (The sums' rounding lets a z_k within 4e-6 of 1 through, far inside
+                // need's 25 % slack; need = 0: 1 / need = inf, 0 * inf = NaN -> sat 0.)
+                static_assert(kK == 16, "sixteen centroids");
+                const float b1 =
+                    fminf(fminf(fminf(fminf(sv[r][0].x, sv[r][0].y), sv[r][1].x),
+                                fminf(fminf(sv[r][1].y, sv[r][2].x), sv[r][2].y)),
+                          fminf(fminf(fminf(fminf(sv[r][3].x, sv[r][3].y), sv[r][4].x),
+                                      fminf(fminf(sv[r][4].y, sv[r][5].x), sv[r][5].y)),
+                                fminf(fminf(fminf(sv[r][6].x, sv[r][6].y), sv[r][7].x), sv[r][7].y)));
+                const float need3 = __fmaf_rn(kN4, fabsf(b1), __fmaf_rn(kN3, x2p[r].x + x2p[r].y, c2));
+                float rneed;
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rneed) : "f"(need3));
+                const float2 nb = make_float2(-b1, -b1);
+                float2 zs[kK / 2];
+                float tsum = 0.f;
+#pragma unroll
+                for (int p = 0; p < kK / 2; ++p) {
+                    const float2 y = __fadd2_rn(sv[r][p], nb);
+                    asm("mul.rn.sat.f32 %0, %1, %2;" : "=f"(zs[p].x) : "f"(y.x), "f"(rneed));
+                    asm("mul.rn.sat.f32 %0, %1, %2;" : "=f"(zs[p].y) : "f"(y.y), "f"(rneed));
+                    if (p > 0) tsum = __fmaf_rn(zs[p].x, (float)(2 * p), tsum);
+                    tsum = __fmaf_rn(zs[p].y, (float)(2 * p + 1), tsum);
+                }
+#pragma unroll
+                for (int w = kK / 4; w >= 1; w /= 2)
+#pragma unroll
+                    for (int p = 0; p < w; ++p) zs[p] = __fadd2_rn(zs[p], zs[p + w]);
+                const bool ambig = !(zs[0].x + zs[0].y >= 15.0f) && valid;
+                const uint32_t arg = valid ? ((uint32_t)__float2int_rn(120.0f - tsum) & 0xFu) : 0u;
+#elif BOLT_ENC_LEAN == 2
                 // Bit-group minima (no index tags): m[j][b] = min of the values whose
                 // index has bit j = b.  The minimum is min(m[j][0], m[j][1]) for any j;
                 // the runner-up differs from the argmin in some bit j, where it is the
@@ -643,7 +677,8 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
                 // |s^_k| <= A = 2 C2 + X2 (2|x.c| <= X2 + ||c||^2), so E = 4 g(L) A
                 // bounds |s^_k - s_k| (2 sum|x_t||c_kt| <= X2 + C2) and the tags move
                 // each value by < 2^-19 A; need' = need + 2 * 2^-19 A (25 % slack)
-#if BOLT_ENC_LEAN == 2
+#if BOLT_ENC_LEAN == 3
+#elif BOLT_ENC_LEAN == 2
                 // the same need without the tag term (no tags), as two FFMAs on the
                 // per-codebook constant
                 const float need = __fmaf_rn(kN4, fabsf(b1), __fmaf_rn(kN3, x2p[r].x + x2p[r].y, c2));
