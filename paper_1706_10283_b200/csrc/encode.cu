@@ -281,6 +281,17 @@ __device__ __noinline__ uint32_t direct_argmin(const float* __restrict__ x, cons
 #ifndef BOLT_ENC_FB_SMEM
 #define BOLT_ENC_FB_SMEM 1
 #endif
+// PK (template): a warp's 4-bit codes of a stage go through a byte staging
+// area in shared memory ([codebook][slab][lane]; the fallback overwrites its own
+// byte) and are packed into layout-v1 words once per stage, instead of three
+// shuffle-OR steps and a predicated store per (codebook, row) and atomics in
+// the fallback.  Used for J <= 128 (c2 0.168 -> 0.160 ms); for J = 512 the
+// staging area would cost a stage (3 -> 2), for J = 256 it measured no gain.
+// BOLT_ENC_PACK=0 switches it off (A/B).
+#ifndef BOLT_ENC_PACK
+#define BOLT_ENC_PACK 1
+#endif
+constexpr int kEncPackCb = 2;  // staged codebooks per warp and stage
 
 // (x & mask) | K in one LOP3: with the mask in a register and the 4-bit
 // centroid index as the immediate (ptxas splits the all-immediate form into
@@ -391,7 +402,7 @@ __device__ __noinline__ uint32_t direct_argmin_s(const uint8_t* __restrict__ row
     return arg;
 }
 
-template <int L, int NS, int RT, int W, int H>
+template <int L, int NS, int RT, int W, int H, bool PK = false>
 __global__ void __launch_bounds__(32 * W + 32, 1)
 encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __restrict__ X, int64_t n, int64_t ldx,
                    const float* __restrict__ C, int m, uint32_t* __restrict__ codes, int64_t nblocks, int S,
@@ -431,6 +442,7 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
     uint32_t* tagmask = reinterpret_cast<uint32_t*>(c2max + ((m + 1) & ~1));  // [2]: ~0xF, kept out of ptxas's sight
     uint64_t* full = reinterpret_cast<uint64_t*>(tagmask + 2);
     uint64_t* empty = full + S;
+    uint8_t* const pk = reinterpret_cast<uint8_t*>(empty + S) + (threadIdx.x >> 5) * (kEncPackCb * RT * 32);  // PK only
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int i = 0; i < S; ++i) {
@@ -693,6 +705,9 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
                 const uint32_t arg = valid ? (__float_as_uint(b1) & 0xFu) : 0u;
 #endif
                 amb |= (ambig ? 1u : 0u) << (cc * RT + r);
+                if constexpr (PK) {
+                    pk[(cc * RT + r) * 32 + lane] = (uint8_t)arg;
+                } else {
                 // layout-v1 word of this row's group: 8 consecutive lanes hold its 8 rows
                 uint32_t v = arg << (4 * (lane & 7));
                 v |= __shfl_xor_sync(0xffffffffu, v, 1);
@@ -705,6 +720,7 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
                 const int64_t g = row >> 3;
                 if ((lane & 7) == 0 && g * kRowsPerWord < n && !(xm & 4)) codes[g * m + c] = v;
 #endif
+                }
             }
         }
         // ambiguous (row, codebook) slices: direct differences (the direct
@@ -725,12 +741,29 @@ encode_rows_kernel(const __grid_constant__ CUtensorMap xmap, const float* __rest
 #else
             const uint32_t arg = direct_argmin_g<L>(X + row * ldx + c * L, C + (size_t)c * kK * L);
 #endif
-            const int pos = 4 * (int)(row & 7);
-            uint32_t* w = codes + (row >> 3) * m + c;
-            atomicAnd(w, ~(0xFu << pos));
-            atomicOr(w, arg << pos);
+            if constexpr (PK) {
+                pk[bit * 32 + lane] = (uint8_t)arg;  // bit = cc RT + r: this lane's own byte
+            } else {
+                const int pos = 4 * (int)(row & 7);
+                uint32_t* w = codes + (row >> 3) * m + c;
+                atomicAnd(w, ~(0xFu << pos));
+                atomicOr(w, arg << pos);
+            }
         }
         __syncwarp();
+#if BOLT_ENC_LEAN
+        // word l of the warp = bytes 8 l .. 8 l + 7 of its staging area: codebook
+        // l / (4 RT), slab (l / 4) % RT, rows 8 (l % 4) .. + 7 of the slab
+        if (PK && lane < 4 * RT * cpw && !(xm & 4)) {
+            const uint2 b = reinterpret_cast<const uint2*>(pk)[lane];
+            const uint32_t tl = b.x | (b.x >> 4), th = b.y | (b.y >> 4);  // byte 0 = b0 | b1 << 4, byte 2 = b2 | b3 << 4
+            const uint32_t v = __byte_perm(tl, th, 0x6420);
+            const int cc = lane / (4 * RT), r = (lane >> 2) % RT;
+            const int lrow0 = 32 * ((warp % SG) * RT + r) + 8 * (lane & 3);
+            if (lrow0 < nrem) cst[(lrow0 >> 3) * m + c0 + (warp / SG) * cpw + cc] = v;
+        }
+        if constexpr (PK) __syncwarp();
+#endif
         if (lane == 0) tc::mbar_arrive(&empty[s]);  // this warp is done with the stage
     }
 }
@@ -779,13 +812,15 @@ cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const f
         const int jh = j / H;
         const int NS = jh <= 128 ? 4 : 2;
         int W = 16, RT = 2;
+        const bool pack = BOLT_ENC_PACK && BOLT_ENC_LEAN && L == 8 && NS == 4 && H == 1;
 #ifdef BOLT_XMODE
         if (getenv("BOLT_ENC_W8") && NS == 4) W = 8, RT = 4;
 #endif
         const int R = 32 * NS;
         const size_t stage = (size_t)R * jh * sizeof(float);
         const size_t tables = (size_t)j * kK * sizeof(float) + (size_t)m * kK * sizeof(float) +
-                              (size_t)(((m + 1) & ~1) + 2) * sizeof(float);  // + the tag mask word
+                              (size_t)(((m + 1) & ~1) + 2) * sizeof(float) +  // + the tag mask word
+                              (pack ? (size_t)(W + 1) * kEncPackCb * RT * 32 : 0);  // code staging, per warp
         const size_t budget = 227 * 1024 - 256;
         int S = (int)std::min<size_t>(4, (budget - tables - 8 * sizeof(uint64_t)) / stage);
         int xm = 0;
@@ -798,7 +833,7 @@ cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const f
         const cuuint64_t strides[1] = {(cuuint64_t)(ldx * sizeof(float))};
         const cuuint32_t box[2] = {32u, (cuuint32_t)R};
         const cuuint32_t estr[2] = {1u, 1u};
-        if (S >= 2 && ((m / H) * (NS / RT)) % W == 0 && n < (int64_t(1) << 31) &&
+        if (S >= 2 && ((m / H) * (NS / RT)) % W == 0 && (!pack || (m / H) * (NS / RT) / W <= kEncPackCb) && n < (int64_t(1) << 31) &&
             encode_tiled()(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box,
                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
@@ -807,7 +842,8 @@ cudaError_t launch_encode(const float* X, int64_t n, int j, int64_t ldx, const f
             const unsigned grid = (unsigned)std::min<int64_t>(nblocks, sms);
             decltype(&encode_rows_kernel<8, 4, 2, 16, 1>) kern;
             if (L == 8) kern = H == 2 ? encode_rows_kernel<8, 2, 2, 16, 2>
-                             : NS == 4 ? (W == 8 ? encode_rows_kernel<8, 4, 4, 8, 1> : encode_rows_kernel<8, 4, 2, 16, 1>)
+                             : NS == 4 ? (W == 8 ? encode_rows_kernel<8, 4, 4, 8, 1>
+                                          : pack ? encode_rows_kernel<8, 4, 2, 16, 1, true> : encode_rows_kernel<8, 4, 2, 16, 1>)
                                        : encode_rows_kernel<8, 2, 2, 16, 1>;
             else kern = H == 2 ? encode_rows_kernel<16, 2, 2, 16, 2>
                         : NS == 4 ? encode_rows_kernel<16, 4, 2, 16, 1> : encode_rows_kernel<16, 2, 2, 16, 1>;
