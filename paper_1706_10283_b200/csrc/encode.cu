@@ -273,11 +273,16 @@ __device__ __noinline__ uint32_t direct_argmin(const float* __restrict__ x, cons
     return arg;
 }
 
-// A/B switch (tools/): 0 rebuilds the round-2 epilogue (two LOP3 per tag,
-// 64-bit row arithmetic per stored word)
+// Argmin epilogue of the expanded kernel (A/B switch, tools/gpu_ab_enc*.sh;
+// DESIGN.md 6.3 has the measurements):
+//   2 (default) bit-group minima, no index tags, need as two FFMAs
+//   3           runner-up test and argmin on the FMA pipe (slower)
+//   1           index tags, one LOP3 each, 32-bit row arithmetic
+//   0           round 2's first epilogue (two LOP3 per tag, 64-bit row arithmetic)
 #ifndef BOLT_ENC_LEAN
 #define BOLT_ENC_LEAN 2
 #endif
+// 1: the direct-difference fallback reads x and the centroids from shared memory
 #ifndef BOLT_ENC_FB_SMEM
 #define BOLT_ENC_FB_SMEM 1
 #endif
